@@ -1,0 +1,144 @@
+/*
+ * hlf_b200.h -- C-ABI of the B200-native Hermite-leapfrog hot path
+ * (arXiv 1808.10481).  Plain pointers and sizes only; no CUDA or torch types.
+ *
+ * The reference (/root/reference/proj) is a C++20 library with no plugin
+ * registry or FFI; its boundary for this path is the C++ API in
+ * proj/include/hlf.  Each entry point below replaces one piece of it:
+ *
+ *   hlf_build_interp_operator  <- hlf::build_interp_operator    interpolation.hpp:22, interpolation.cpp:21-51
+ *   hlf_create                 <- hlf::Stepper1d::Stepper1d     stepper1d.hpp:68, stepper1d.cpp:93-111
+ *                                 (+ Grid1d/Grid2d::over grid.hpp:12,29; SchemeConfig::validate config.hpp:37)
+ *   hlf_set_field/get_field    <- State1d::p / State1d::v       stepper1d.hpp:49-52 (public, caller-owned jets)
+ *   hlf_set_times/get_times    <- State1d::t_p, t_v, dt         stepper1d.hpp:50
+ *   hlf_set_dt                 <- `st.dt = -dt` (time reversal) tests/test_stepper1d.cpp:288
+ *   hlf_set_coeff              <- Stepper1d::ap_prim_/ap_dual_  stepper1d.cpp:103-110 (coefficient jets)
+ *   hlf_advance_p              <- Stepper1d::advance_p          stepper1d.hpp:72, stepper1d.cpp:147-156
+ *   hlf_advance_v              <- Stepper1d::advance_v          stepper1d.hpp:73, stepper1d.cpp:158-166
+ *   hlf_step                   <- Stepper1d::step_system        stepper1d.hpp:74, stepper1d.cpp:168-172
+ *   hlf_advance_n              <- the caller's step loop        tests/test_stepper1d.cpp:38
+ *   hlf_poll_finite            <- Stepper1d::check_finite       stepper1d.cpp:121-129
+ *   status codes               <- ConfigError, InstabilityError config.hpp:15-24, std::invalid_argument
+ *
+ * Fields: 0 = p on the primary grid; 1..d = velocity components on the dual
+ * grid (Problem2d field order p, v, u: problem.hpp:41-46).  Host buffers are
+ * AoS [node][coef]: node (ix, iy, iz) -> ((ix*Ny)+iy)*Nz+iz, coefficient
+ * (a, b, c) -> (a*(m+1)+b)*(m+1)+c -- both x-major like TensorJet::at
+ * (jet.hpp:43-44) and PiecewiseTensor::cell (interpolation.hpp:50-52).
+ * Primary grid: K nodes per periodic axis, K+1 per reflective axis (walls on
+ * primary lines); dual grid: K per axis.
+ */
+#ifndef HLF_B200_H
+#define HLF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hlf_status {
+  HLF_OK = 0,
+  HLF_CONFIG_ERROR = 1,     /* hlf::ConfigError        (config.hpp:15-17) */
+  HLF_INSTABILITY = 2,      /* hlf::InstabilityError   (config.hpp:19-24) */
+  HLF_INVALID_ARGUMENT = 3, /* std::invalid_argument   (interpolation.cpp:65-66) */
+  HLF_CUDA_ERROR = 4,
+  HLF_NCCL_ERROR = 5
+} hlf_status;
+
+enum { HLF_PERIODIC = 0, HLF_REFLECTIVE = 1 }; /* hlf::Boundary (config.hpp:10) */
+enum { HLF_PRIMARY = 0, HLF_DUAL = 1 };
+
+/* Version of this ABI; bump on any signature change. */
+#define HLF_B200_ABI_VERSION 1
+
+typedef struct hlf_solver hlf_solver; /* opaque */
+
+typedef struct hlf_desc {
+  int dim;            /* 1, 2 or 3 */
+  int m;              /* order, [0, SchemeConfig::m_cap = 8]; device kernels: d<=2 any m, d=3 m<=4 */
+  int K[3];           /* cells per axis (unused axes ignored); K >= 2 (grid.cpp:10) */
+  double x_min[3];    /* lower domain corner (primary node 0) */
+  double h;           /* common spacing (Grid1d::h; Grid2d is square, grid.cpp:25-26) */
+  int boundary[3];    /* HLF_PERIODIC / HLF_REFLECTIVE per axis */
+  double ap, av;      /* constant coefficients: p_t = ap div v, v_t = av grad p (problem.hpp:11-14,36-38) */
+  int variable_ap;    /* 1: per-node ap jets (e.g. -c^2(x)) are supplied with hlf_set_coeff */
+  const double* M;    /* (2m+2)^2 row-major interpolation operator; NULL = build it here */
+  int device;         /* CUDA ordinal */
+  void* stream;       /* cudaStream_t to launch on; NULL = the library's own stream */
+  int z_slab;         /* 1: z is one slab of a periodic decomposition; z halos come
+                         from hlf_halo_* instead of the local wrap */
+} hlf_desc;
+
+/* --- interpolation operator ---------------------------------------------- */
+/* M = A^{-1} (row-major, (2m+2)^2) and its 1-norm condition; HLF_CONFIG_ERROR for m outside [0, 8] */
+hlf_status hlf_build_interp_operator(int m, double* M_out, double* condition_out);
+
+/* --- lifetime ------------------------------------------------------------ */
+hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out);
+void hlf_destroy(hlf_solver* s);
+/* message of the last failing call on this handle (or of the last failing
+   hlf_create on this thread when s is NULL) */
+const char* hlf_last_error(const hlf_solver* s);
+int hlf_abi_version(void);
+
+/* --- geometry ------------------------------------------------------------ */
+int64_t hlf_num_nodes(const hlf_solver* s, int grid);     /* real nodes (no ghosts) */
+int hlf_num_coeffs(const hlf_solver* s);                  /* (m+1)^d */
+
+/* --- staggered state ----------------------------------------------------- */
+hlf_status hlf_set_field(hlf_solver* s, int field, const double* host_aos);
+hlf_status hlf_get_field(hlf_solver* s, int field, double* host_aos);
+/* per-node ap jets, (2m+2)^d entries per node (x-major), for grid HLF_PRIMARY / HLF_DUAL */
+hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets);
+hlf_status hlf_set_times(hlf_solver* s, double t_p, double t_v, double dt);
+hlf_status hlf_get_times(const hlf_solver* s, double* t_p, double* t_v, double* dt);
+hlf_status hlf_set_dt(hlf_solver* s, double dt);
+
+/* --- stepping (asynchronous on the solver's stream) ---------------------- */
+hlf_status hlf_advance_p(hlf_solver* s);
+hlf_status hlf_advance_v(hlf_solver* s);
+/* advance_p, advance_v, finite check: HLF_INSTABILITY (synchronous) if the
+   state became non-finite; message "solution became non-finite at step N" */
+hlf_status hlf_step(hlf_solver* s, int step_index);
+/* n steps indexed first..first+n-1; the finite flag is read once at the end and
+   the first offending step index is reported through HLF_INSTABILITY */
+hlf_status hlf_advance_n(hlf_solver* s, int n, int first_step);
+/* -1 when the state stayed finite, else the first non-finite step index */
+hlf_status hlf_poll_finite(hlf_solver* s, int* first_bad_step);
+hlf_status hlf_clear_finite(hlf_solver* s);
+hlf_status hlf_synchronize(hlf_solver* s);
+
+/* --- device-resident data (no host copies) ------------------------------- */
+/* device base of a field, SoA [layer][coef][y][x] (layer includes z ghosts:
+   p layer index = z, v layer index = z + 1); strides in elements */
+hlf_status hlf_field_device(hlf_solver* s, int field, double** dev_ptr, int64_t* layer_stride,
+                            int64_t* coef_stride, int* layers);
+/* field += amp * prod_ax sin(w[ax] x_ax + phase[ax]) as exact scaled jets at the
+   field's nodes (sin_jet, jet.cpp:65-74), computed on the device */
+hlf_status hlf_fill_separable(hlf_solver* s, int field, double amp, const double* w,
+                              const double* phase);
+hlf_status hlf_zero_field(hlf_solver* s, int field);
+
+/* --- z-slab halos (multi-GPU; z_slab = 1) -------------------------------- */
+/* The velocity half step reads p layer Kz (the next rank's layer 0); the
+   pressure half step reads v layer -1 (the previous rank's layer Kz-1).
+   hlf_halo_send_ptr gives the device pointer of the layer this rank must
+   send, hlf_halo_recv_ptr where the received layer must land, both
+   layer_stride doubles long.  kind 0 = p halo (before advance_v), 1 = v halo
+   of component c (before advance_p). */
+hlf_status hlf_halo_send_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr, int64_t* count);
+hlf_status hlf_halo_recv_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr, int64_t* count);
+
+/* number of kernels this solver has launched (for launch accounting) */
+int64_t hlf_launch_count(const hlf_solver* s);
+/* kernel variant the next half steps use: 0 generic, 1 tiled 3D */
+int hlf_kernel_variant(const hlf_solver* s);
+hlf_status hlf_set_kernel_variant(hlf_solver* s, int variant);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HLF_B200_H */

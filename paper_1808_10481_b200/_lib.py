@@ -1,0 +1,99 @@
+"""ctypes binding of the product library ``lib/libhlf_b200.so`` (C-ABI in
+include/hlf_b200.h).  There is no fallback: if the shared library is missing
+the import fails loudly."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libhlf_b200.so")
+
+HLF_OK = 0
+HLF_CONFIG_ERROR = 1
+HLF_INSTABILITY = 2
+HLF_INVALID_ARGUMENT = 3
+HLF_CUDA_ERROR = 4
+HLF_NCCL_ERROR = 5
+
+# every exported symbol declared in include/hlf_b200.h
+EXPORTS = [
+    "hlf_abi_version", "hlf_build_interp_operator", "hlf_create", "hlf_destroy", "hlf_last_error",
+    "hlf_num_nodes", "hlf_num_coeffs", "hlf_set_field", "hlf_get_field", "hlf_set_coeff",
+    "hlf_set_times", "hlf_get_times", "hlf_set_dt", "hlf_advance_p", "hlf_advance_v", "hlf_step",
+    "hlf_advance_n", "hlf_poll_finite", "hlf_clear_finite", "hlf_synchronize", "hlf_field_device",
+    "hlf_fill_separable", "hlf_zero_field", "hlf_halo_send_ptr", "hlf_halo_recv_ptr",
+    "hlf_launch_count", "hlf_kernel_variant", "hlf_set_kernel_variant",
+]
+
+
+class HlfDesc(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int),
+        ("m", C.c_int),
+        ("K", C.c_int * 3),
+        ("x_min", C.c_double * 3),
+        ("h", C.c_double),
+        ("boundary", C.c_int * 3),
+        ("ap", C.c_double),
+        ("av", C.c_double),
+        ("variable_ap", C.c_int),
+        ("M", C.POINTER(C.c_double)),
+        ("device", C.c_int),
+        ("stream", C.c_void_p),
+        ("z_slab", C.c_int),
+    ]
+
+
+_dp = C.POINTER(C.c_double)
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA extension (python -c 'import __graft_entry__ as g; g.build()')"
+        )
+    L = C.CDLL(LIB_PATH)
+    S = C.c_void_p
+    st = C.c_int
+    sig = {
+        "hlf_abi_version": ([], C.c_int),
+        "hlf_build_interp_operator": ([C.c_int, _dp, _dp], st),
+        "hlf_create": ([C.POINTER(HlfDesc), C.POINTER(C.c_void_p)], st),
+        "hlf_destroy": ([S], None),
+        "hlf_last_error": ([S], C.c_char_p),
+        "hlf_num_nodes": ([S, C.c_int], C.c_int64),
+        "hlf_num_coeffs": ([S], C.c_int),
+        "hlf_set_field": ([S, C.c_int, C.c_void_p], st),
+        "hlf_get_field": ([S, C.c_int, C.c_void_p], st),
+        "hlf_set_coeff": ([S, C.c_int, C.c_void_p], st),
+        "hlf_set_times": ([S, C.c_double, C.c_double, C.c_double], st),
+        "hlf_get_times": ([S, _dp, _dp, _dp], st),
+        "hlf_set_dt": ([S, C.c_double], st),
+        "hlf_advance_p": ([S], st),
+        "hlf_advance_v": ([S], st),
+        "hlf_step": ([S, C.c_int], st),
+        "hlf_advance_n": ([S, C.c_int, C.c_int], st),
+        "hlf_poll_finite": ([S, C.POINTER(C.c_int)], st),
+        "hlf_clear_finite": ([S], st),
+        "hlf_synchronize": ([S], st),
+        "hlf_field_device": ([S, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                              C.POINTER(C.c_int)], st),
+        "hlf_fill_separable": ([S, C.c_int, C.c_double, _dp, _dp], st),
+        "hlf_zero_field": ([S, C.c_int], st),
+        "hlf_halo_send_ptr": ([S, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)], st),
+        "hlf_halo_recv_ptr": ([S, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)], st),
+        "hlf_launch_count": ([S], C.c_int64),
+        "hlf_kernel_variant": ([S], C.c_int),
+        "hlf_set_kernel_variant": ([S, C.c_int], st),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L

@@ -1,0 +1,624 @@
+// Host orchestration behind the C-ABI in include/hlf_b200.h.
+//
+// Owns the device-resident staggered state (SoA [layer][coef][y][x] per
+// field), the CK weights for the current dt, the z ghost layers, and the
+// fused non-finite flag.  Mirrors the reference's Stepper1d semantics
+// (proj/src/stepper1d.cpp): advance_p then advance_v, time stamps advanced by
+// += dt on the host (:155, :165), InstabilityError carrying the step index
+// (:121-129), ConfigError for bad m / grid / field count (config.cpp:27-32,
+// grid.cpp:10-26).
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hlf_b200.h"
+#include "hlf_internal.cuh"
+
+using hlfk::HalfParams;
+
+struct hlf_solver {
+  int d = 1, m = 0, n1 = 1, n = 2, F = 1, E = 1;
+  int K[3] = {1, 1, 1};
+  int bnd[3] = {0, 0, 0};
+  int Np[3] = {1, 1, 1}, Nd[3] = {1, 1, 1};
+  double x_min[3] = {0, 0, 0};
+  double h = 1.0, ap = -1.0, av = -1.0;
+  bool variable = false;
+  bool z_slab = false;
+  double t_p = 0.0, t_v = 0.0, dt = 0.0;
+  std::vector<double> M;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // fields: 0 = p, 1..d = v components
+  double* field[4] = {nullptr, nullptr, nullptr, nullptr};
+  int layers[4] = {1, 1, 1, 1};
+  int64_t plane[4] = {1, 1, 1, 1};
+  double* coeff[2] = {nullptr, nullptr};
+  int* flag = nullptr;
+  int* flag_host = nullptr;
+  double* staging = nullptr;
+  size_t staging_bytes = 0;
+  int64_t launches = 0;
+  int variant = 0;
+  std::string err;
+
+  int64_t layer_stride(int f) const { return plane[f] * F; }
+  int zoff(int f) const { return (d == 3 && f > 0) ? 1 : 0; }
+  int grid_of(int f) const { return f == 0 ? HLF_PRIMARY : HLF_DUAL; }
+  const int* nodes_of(int f) const { return f == 0 ? Np : Nd; }
+  int64_t num_nodes(int grid) const {
+    const int* N = grid == HLF_PRIMARY ? Np : Nd;
+    return static_cast<int64_t>(N[0]) * N[1] * N[2];
+  }
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+hlf_status fail(hlf_solver* s, hlf_status st, const std::string& msg) {
+  if (s) s->err = msg;
+  else g_create_error = msg;
+  return st;
+}
+
+hlf_status cuda_fail(hlf_solver* s, cudaError_t e, const char* what) {
+  return fail(s, HLF_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define HLF_CUDA(s, call)                                      \
+  do {                                                         \
+    cudaError_t hlf_e_ = (call);                               \
+    if (hlf_e_ != cudaSuccess) return cuda_fail((s), hlf_e_, #call); \
+  } while (0)
+
+double binom(int s, int l) {
+  double b = 1.0;
+  for (int q = 0; q < l; ++q) b = b * (s - q) / (q + 1);
+  return b;
+}
+
+// M = A^{-1} by Gauss-Jordan with partial pivoting (the algorithm of
+// Eigen::PartialPivLU::inverse used at interpolation.cpp:40).
+void build_M(int m, std::vector<double>& M, double* cond) {
+  const int n = 2 * m + 2;
+  std::vector<double> A(static_cast<size_t>(n) * n, 0.0), W, inv(static_cast<size_t>(n) * n, 0.0);
+  for (int half = 0; half < 2; ++half) {
+    const double xi = half == 0 ? -0.5 : 0.5;
+    for (int l = 0; l <= m; ++l) {
+      const int row = half * (m + 1) + l;
+      for (int s = l; s < n; ++s) A[row * n + s] = binom(s, l) * std::pow(xi, s - l);
+    }
+  }
+  W = A;
+  for (int i = 0; i < n; ++i) inv[i * n + i] = 1.0;
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < n; ++r)
+      if (std::abs(W[r * n + col]) > std::abs(W[piv * n + col])) piv = r;
+    if (piv != col)
+      for (int j = 0; j < n; ++j) {
+        std::swap(W[piv * n + j], W[col * n + j]);
+        std::swap(inv[piv * n + j], inv[col * n + j]);
+      }
+    const double dd = W[col * n + col];
+    for (int j = 0; j < n; ++j) {
+      W[col * n + j] /= dd;
+      inv[col * n + j] /= dd;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == col) continue;
+      const double f = W[r * n + col];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        W[r * n + j] -= f * W[col * n + j];
+        inv[r * n + j] -= f * inv[col * n + j];
+      }
+    }
+  }
+  M = inv;
+  if (cond) {
+    auto norm1 = [n](const std::vector<double>& X) {
+      double best = 0.0;
+      for (int j = 0; j < n; ++j) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += std::abs(X[i * n + j]);
+        best = s > best ? s : best;
+      }
+      return best;
+    };
+    *cond = norm1(A) * norm1(inv);
+  }
+}
+
+int ipow(int b, int e) {
+  int r = 1;
+  while (e-- > 0) r *= b;
+  return r;
+}
+
+bool valid_field(const hlf_solver* s, int f) { return f >= 0 && f <= s->d; }
+
+hlf_status ensure_staging(hlf_solver* s, size_t bytes) {
+  if (s->staging_bytes >= bytes) return HLF_OK;
+  if (s->staging) cudaFree(s->staging);
+  s->staging = nullptr;
+  s->staging_bytes = 0;
+  HLF_CUDA(s, cudaMalloc(&s->staging, bytes));
+  s->staging_bytes = bytes;
+  return HLF_OK;
+}
+
+constexpr size_t kChunkBytes = size_t(256) << 20;
+
+// host AoS [node][per] <-> device SoA [zoff+z][per][y][x], through a device
+// staging chunk (one H2D/D2H copy + one permute kernel per chunk)
+hlf_status transfer(hlf_solver* s, double* dev, const int* N, int per, int64_t layer, int zoff,
+                    double* host, bool to_device) {
+  const int64_t nodes = static_cast<int64_t>(N[0]) * N[1] * N[2];
+  const int64_t chunk_nodes = std::max<int64_t>(1, static_cast<int64_t>(kChunkBytes / (sizeof(double) * per)));
+  hlf_status st = ensure_staging(s, std::min<int64_t>(nodes, chunk_nodes) * per * sizeof(double));
+  if (st != HLF_OK) return st;
+  const int64_t coef = static_cast<int64_t>(N[0]) * N[1];
+  for (int64_t n0 = 0; n0 < nodes; n0 += chunk_nodes) {
+    const int64_t cnt = std::min(chunk_nodes, nodes - n0);
+    const size_t bytes = static_cast<size_t>(cnt) * per * sizeof(double);
+    if (to_device) {
+      HLF_CUDA(s, cudaMemcpyAsync(s->staging, host + n0 * per, bytes, cudaMemcpyHostToDevice, s->stream));
+      s->launches += hlfk::launch_aos_to_soa(s->staging, dev, n0, cnt, per, N[0], N[1], N[2], layer, coef,
+                                             zoff, s->stream);
+    } else {
+      s->launches += hlfk::launch_soa_to_aos(dev, s->staging, n0, cnt, per, N[0], N[1], N[2], layer, coef,
+                                             zoff, s->stream);
+      HLF_CUDA(s, cudaMemcpyAsync(host + n0 * per, s->staging, bytes, cudaMemcpyDeviceToHost, s->stream));
+    }
+    HLF_CUDA(s, cudaGetLastError());
+  }
+  HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+  return HLF_OK;
+}
+
+// z ghost layers for d = 3 (skipped in slab mode: the caller exchanges halos)
+hlf_status fill_ghosts(hlf_solver* s, bool for_pressure) {
+  if (s->d != 3 || s->z_slab) return HLF_OK;
+  const int Kz = s->K[2];
+  if (!for_pressure) {
+    // velocity half step reads p layer Kz: periodic wrap = copy of layer 0
+    if (s->bnd[2] == HLF_PERIODIC) {
+      const int64_t L = s->layer_stride(0);
+      HLF_CUDA(s, cudaMemcpyAsync(s->field[0] + Kz * L, s->field[0], L * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s->stream));
+    }
+    return HLF_OK;
+  }
+  for (int c = 1; c <= 3; ++c) {
+    const int64_t L = s->layer_stride(c);
+    double* base = s->field[c];
+    if (s->bnd[2] == HLF_PERIODIC) {
+      // ghost index 0 (z = -1) = layer z = Kz-1 (index Kz)
+      HLF_CUDA(s, cudaMemcpyAsync(base, base + Kz * L, L * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  s->stream));
+    } else {
+      const double sigma = (c - 1) == 2 ? 1.0 : -1.0;  // wall-normal v_z even, tangential odd
+      s->launches += hlfk::launch_mirror_layer(base, base + L, s->plane[c], s->n1, 3, sigma, s->stream);
+      s->launches += hlfk::launch_mirror_layer(base + (Kz + 1) * L, base + Kz * L, s->plane[c], s->n1, 3,
+                                               sigma, s->stream);
+    }
+  }
+  HLF_CUDA(s, cudaGetLastError());
+  return HLF_OK;
+}
+
+void fill_weights(const hlf_solver* s, hlfk::HalfKind kind, HalfParams& P) {
+  std::memcpy(P.M, s->M.data(), sizeof(double) * s->M.size());
+  // w_r = 2 prod_{q<=r} (dt/2)/q, exactly as leapfrog_half_update (stepper1d.cpp:57-58)
+  for (int r = 0; r < s->n && r < hlfk::kMaxN; ++r) {
+    double w = 2.0;
+    for (int q = 1; q <= r; ++q) w *= s->dt / 2.0 / q;
+    P.w[r] = w;
+  }
+  for (int k = 0; k <= s->m; ++k) {
+    const int r = 2 * k + 1;
+    double g = P.w[r];
+    for (int q = 0; q < r; ++q) g /= s->h;
+    const double a_pow = kind == hlfk::VEL ? std::pow(s->av, k + 1) * std::pow(s->ap, k)
+                                           : std::pow(s->ap, k + 1) * std::pow(s->av, k);
+    P.G[k] = g * a_pow;
+  }
+  P.inv_h = 1.0 / s->h;
+  P.ap = s->ap;
+  P.av = s->av;
+}
+
+hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step) {
+  hlf_status st = fill_ghosts(s, kind == hlfk::PRE);
+  if (st != HLF_OK) return st;
+  HalfParams P;
+  std::memset(&P, 0, sizeof(P));
+  fill_weights(s, kind, P);
+  const int tf = kind == hlfk::VEL ? 1 : 0;  // first target field
+  const int sf = kind == hlfk::VEL ? 0 : 1;  // first source field
+  const int* tN = s->nodes_of(tf);
+  const int* sN = s->nodes_of(sf);
+  for (int c = 0; c < 3; ++c) {
+    P.src[c] = c < (kind == hlfk::VEL ? 1 : s->d) ? s->field[sf + c] : nullptr;
+    P.dst[c] = c < (kind == hlfk::VEL ? s->d : 1) ? s->field[tf + c] : nullptr;
+    P.K[c] = s->K[c];
+    P.bnd[c] = s->bnd[c];
+  }
+  P.s_layer = s->layer_stride(sf);
+  P.s_coef = s->plane[sf];
+  P.t_layer = s->layer_stride(tf);
+  P.t_coef = s->plane[tf];
+  P.sNx = sN[0];
+  P.sNy = sN[1];
+  P.tNx = tN[0];
+  P.tNy = tN[1];
+  P.tNz = tN[2];
+  P.t_zoff = s->zoff(tf);
+  P.s_zoff = s->zoff(sf);
+  P.coeff = s->variable ? s->coeff[s->grid_of(tf)] : nullptr;
+  P.c_coef = s->plane[tf];
+  P.c_layer = s->plane[tf] * s->E;
+  P.step = step;
+  P.flag = s->flag;
+  int launched = -1;
+  if (s->variant == 1 && !s->variable && s->d == 3 && hlfk::tiled3d_supported(s->m))
+    launched = hlfk::launch_half_tiled3d(s->m, kind, P, s->stream);
+  else
+    launched = hlfk::launch_half_generic(s->d, s->m, s->variable, kind, P, s->stream);
+  if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
+  s->launches += launched;
+  HLF_CUDA(s, cudaGetLastError());
+  return HLF_OK;
+}
+
+hlf_status read_flag(hlf_solver* s, int* bad) {
+  HLF_CUDA(s, cudaMemcpyAsync(s->flag_host, s->flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+  *bad = *s->flag_host == INT_MAX ? -1 : *s->flag_host;
+  return HLF_OK;
+}
+
+hlf_status instability(hlf_solver* s, int step) {
+  return fail(s, HLF_INSTABILITY, "solution became non-finite at step " + std::to_string(step));
+}
+
+}  // namespace
+
+extern "C" {
+
+int hlf_abi_version(void) { return HLF_B200_ABI_VERSION; }
+
+hlf_status hlf_build_interp_operator(int m, double* M_out, double* condition_out) {
+  if (m < 0 || m > hlfk::kMaxM)
+    return fail(nullptr, HLF_CONFIG_ERROR, "interpolation order m must be in [0, 8]");
+  std::vector<double> M;
+  build_M(m, M, condition_out);
+  if (M_out) std::memcpy(M_out, M.data(), sizeof(double) * M.size());
+  return HLF_OK;
+}
+
+hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
+  if (!desc || !out) return fail(nullptr, HLF_INVALID_ARGUMENT, "null descriptor");
+  *out = nullptr;
+  const int d = desc->dim;
+  if (d < 1 || d > 3) return fail(nullptr, HLF_CONFIG_ERROR, "dim must be 1, 2 or 3");
+  if (desc->m < 0 || desc->m > hlfk::kMaxM)
+    return fail(nullptr, HLF_CONFIG_ERROR, "scheme order m must be in [0, 8]");
+  if (d == 3 && desc->m > 4)
+    return fail(nullptr, HLF_CONFIG_ERROR, "3D device kernels support m <= 4");
+  if (!(desc->h > 0.0) || !std::isfinite(desc->h))
+    return fail(nullptr, HLF_CONFIG_ERROR, "grid spacing must be positive");
+  for (int ax = 0; ax < d; ++ax) {
+    if (desc->K[ax] < 2) return fail(nullptr, HLF_CONFIG_ERROR, "grid needs K >= 2");
+    if (desc->boundary[ax] != HLF_PERIODIC && desc->boundary[ax] != HLF_REFLECTIVE)
+      return fail(nullptr, HLF_CONFIG_ERROR, "unknown boundary kind");
+  }
+  if (desc->z_slab && (d != 3 || desc->boundary[2] != HLF_PERIODIC))
+    return fail(nullptr, HLF_CONFIG_ERROR, "z slabs need d = 3 with a periodic z axis");
+
+  hlf_solver* s = new hlf_solver;
+  s->d = d;
+  s->m = desc->m;
+  s->n1 = desc->m + 1;
+  s->n = 2 * desc->m + 2;
+  s->F = ipow(s->n1, d);
+  s->E = ipow(s->n, d);
+  s->h = desc->h;
+  s->ap = desc->ap;
+  s->av = desc->av;
+  s->variable = desc->variable_ap != 0;
+  s->z_slab = desc->z_slab != 0;
+  s->device = desc->device;
+  for (int ax = 0; ax < 3; ++ax) {
+    const bool used = ax < d;
+    s->K[ax] = used ? desc->K[ax] : 1;
+    s->bnd[ax] = used ? desc->boundary[ax] : HLF_PERIODIC;
+    s->x_min[ax] = used ? desc->x_min[ax] : 0.0;
+    s->Nd[ax] = s->K[ax];
+    s->Np[ax] = used && s->bnd[ax] == HLF_REFLECTIVE ? s->K[ax] + 1 : s->K[ax];
+  }
+  if (desc->M) {
+    s->M.assign(desc->M, desc->M + s->n * s->n);
+  } else {
+    build_M(s->m, s->M, nullptr);
+  }
+  auto bail = [&](hlf_status st) {
+    g_create_error = s->err;
+    hlf_destroy(s);
+    return st;
+  };
+  cudaError_t e = cudaSetDevice(s->device);
+  if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaSetDevice"));
+  if (desc->stream) {
+    s->stream = static_cast<cudaStream_t>(desc->stream);
+  } else {
+    e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaStreamCreate"));
+    s->own_stream = true;
+  }
+  for (int f = 0; f <= d; ++f) {
+    const int* N = s->nodes_of(f);
+    s->plane[f] = static_cast<int64_t>(N[0]) * N[1];
+    // d = 3: p gets one upper ghost/halo layer unless the z walls already
+    // provide node Kz; every v component gets a ghost layer on each side
+    s->layers[f] = d == 3 ? (f == 0 ? s->K[2] + 1 : s->K[2] + 2) : 1;
+    const size_t bytes = static_cast<size_t>(s->layers[f]) * s->layer_stride(f) * sizeof(double);
+    e = cudaMalloc(&s->field[f], bytes);
+    if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaMalloc(field)"));
+    e = cudaMemsetAsync(s->field[f], 0, bytes, s->stream);
+    if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaMemset(field)"));
+  }
+  e = cudaMalloc(&s->flag, sizeof(int));
+  if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaMalloc(flag)"));
+  e = cudaMallocHost(&s->flag_host, sizeof(int));
+  if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaMallocHost(flag)"));
+  const int big = INT_MAX;
+  e = cudaMemcpyAsync(s->flag, &big, sizeof(int), cudaMemcpyHostToDevice, s->stream);
+  if (e != cudaSuccess) return bail(cuda_fail(s, e, "flag init"));
+  e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return bail(cuda_fail(s, e, "sync"));
+  s->variant = (d == 3 && !s->variable && hlfk::tiled3d_supported(s->m)) ? 1 : 0;
+  *out = s;
+  return HLF_OK;
+}
+
+void hlf_destroy(hlf_solver* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  for (double*& f : s->field)
+    if (f) cudaFree(f);
+  for (double*& c : s->coeff)
+    if (c) cudaFree(c);
+  if (s->flag) cudaFree(s->flag);
+  if (s->flag_host) cudaFreeHost(s->flag_host);
+  if (s->staging) cudaFree(s->staging);
+  if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+const char* hlf_last_error(const hlf_solver* s) { return s ? s->err.c_str() : g_create_error.c_str(); }
+
+int64_t hlf_num_nodes(const hlf_solver* s, int grid) { return s ? s->num_nodes(grid) : -1; }
+int hlf_num_coeffs(const hlf_solver* s) { return s ? s->F : -1; }
+
+hlf_status hlf_set_field(hlf_solver* s, int field, const double* host_aos) {
+  if (!s || !valid_field(s, field) || !host_aos) return fail(s, HLF_INVALID_ARGUMENT, "bad field or buffer");
+  cudaSetDevice(s->device);
+  return transfer(s, s->field[field], s->nodes_of(field), s->F, s->layer_stride(field), s->zoff(field),
+                  const_cast<double*>(host_aos), true);
+}
+
+hlf_status hlf_get_field(hlf_solver* s, int field, double* host_aos) {
+  if (!s || !valid_field(s, field) || !host_aos) return fail(s, HLF_INVALID_ARGUMENT, "bad field or buffer");
+  cudaSetDevice(s->device);
+  return transfer(s, s->field[field], s->nodes_of(field), s->F, s->layer_stride(field), s->zoff(field),
+                  host_aos, false);
+}
+
+hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets) {
+  if (!s || (grid != HLF_PRIMARY && grid != HLF_DUAL) || !host_jets)
+    return fail(s, HLF_INVALID_ARGUMENT, "bad grid or buffer");
+  if (!s->variable) return fail(s, HLF_CONFIG_ERROR, "solver was created with constant coefficients");
+  cudaSetDevice(s->device);
+  const int* N = grid == HLF_PRIMARY ? s->Np : s->Nd;
+  const int64_t plane = static_cast<int64_t>(N[0]) * N[1];
+  if (!s->coeff[grid]) {
+    const size_t bytes = static_cast<size_t>(s->num_nodes(grid)) * s->E * sizeof(double);
+    HLF_CUDA(s, cudaMalloc(&s->coeff[grid], bytes));
+  }
+  return transfer(s, s->coeff[grid], N, s->E, plane * s->E, 0, const_cast<double*>(host_jets), true);
+}
+
+hlf_status hlf_set_times(hlf_solver* s, double t_p, double t_v, double dt) {
+  if (!s) return fail(s, HLF_INVALID_ARGUMENT, "null solver");
+  s->t_p = t_p;
+  s->t_v = t_v;
+  s->dt = dt;
+  return HLF_OK;
+}
+
+hlf_status hlf_get_times(const hlf_solver* s, double* t_p, double* t_v, double* dt) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (t_p) *t_p = s->t_p;
+  if (t_v) *t_v = s->t_v;
+  if (dt) *dt = s->dt;
+  return HLF_OK;
+}
+
+hlf_status hlf_set_dt(hlf_solver* s, double dt) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  s->dt = dt;
+  return HLF_OK;
+}
+
+hlf_status hlf_advance_p(hlf_solver* s) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (s->variable && !s->coeff[HLF_PRIMARY]) return fail(s, HLF_CONFIG_ERROR, "primary-grid ap jets not set");
+  cudaSetDevice(s->device);
+  hlf_status st = launch_half(s, hlfk::PRE, -1);
+  if (st != HLF_OK) return st;
+  s->t_p += s->dt;
+  return HLF_OK;
+}
+
+hlf_status hlf_advance_v(hlf_solver* s) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (s->variable && !s->coeff[HLF_DUAL]) return fail(s, HLF_CONFIG_ERROR, "dual-grid ap jets not set");
+  cudaSetDevice(s->device);
+  hlf_status st = launch_half(s, hlfk::VEL, -1);
+  if (st != HLF_OK) return st;
+  s->t_v += s->dt;
+  return HLF_OK;
+}
+
+static hlf_status step_async(hlf_solver* s, int step_index) {
+  if (s->variable && (!s->coeff[0] || !s->coeff[1])) return fail(s, HLF_CONFIG_ERROR, "ap jets not set");
+  hlf_status st = launch_half(s, hlfk::PRE, step_index);
+  if (st != HLF_OK) return st;
+  s->t_p += s->dt;
+  st = launch_half(s, hlfk::VEL, step_index);
+  if (st != HLF_OK) return st;
+  s->t_v += s->dt;
+  return HLF_OK;
+}
+
+hlf_status hlf_step(hlf_solver* s, int step_index) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  cudaSetDevice(s->device);
+  hlf_status st = step_async(s, step_index);
+  if (st != HLF_OK) return st;
+  int bad = -1;
+  st = read_flag(s, &bad);
+  if (st != HLF_OK) return st;
+  return bad >= 0 ? instability(s, bad) : HLF_OK;
+}
+
+hlf_status hlf_advance_n(hlf_solver* s, int n, int first_step) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (n < 0) return fail(s, HLF_INVALID_ARGUMENT, "negative step count");
+  cudaSetDevice(s->device);
+  for (int i = 0; i < n; ++i) {
+    hlf_status st = step_async(s, first_step + i);
+    if (st != HLF_OK) return st;
+  }
+  int bad = -1;
+  hlf_status st = read_flag(s, &bad);
+  if (st != HLF_OK) return st;
+  return bad >= 0 ? instability(s, bad) : HLF_OK;
+}
+
+hlf_status hlf_poll_finite(hlf_solver* s, int* first_bad_step) {
+  if (!s || !first_bad_step) return HLF_INVALID_ARGUMENT;
+  cudaSetDevice(s->device);
+  return read_flag(s, first_bad_step);
+}
+
+hlf_status hlf_clear_finite(hlf_solver* s) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  cudaSetDevice(s->device);
+  *s->flag_host = INT_MAX;
+  HLF_CUDA(s, cudaMemcpyAsync(s->flag, s->flag_host, sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+  return HLF_OK;
+}
+
+hlf_status hlf_synchronize(hlf_solver* s) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  cudaSetDevice(s->device);
+  HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+  return HLF_OK;
+}
+
+hlf_status hlf_field_device(hlf_solver* s, int field, double** dev_ptr, int64_t* layer_stride,
+                            int64_t* coef_stride, int* layers) {
+  if (!s || !valid_field(s, field)) return fail(s, HLF_INVALID_ARGUMENT, "bad field");
+  if (dev_ptr) *dev_ptr = s->field[field];
+  if (layer_stride) *layer_stride = s->layer_stride(field);
+  if (coef_stride) *coef_stride = s->plane[field];
+  if (layers) *layers = s->layers[field];
+  return HLF_OK;
+}
+
+hlf_status hlf_fill_separable(hlf_solver* s, int field, double amp, const double* w, const double* phase) {
+  if (!s || !valid_field(s, field) || !w || !phase) return fail(s, HLF_INVALID_ARGUMENT, "bad field");
+  cudaSetDevice(s->device);
+  hlfk::FillParams P;
+  std::memset(&P, 0, sizeof(P));
+  const int* N = s->nodes_of(field);
+  P.dst = s->field[field];
+  P.layer = s->layer_stride(field);
+  P.coef = s->plane[field];
+  P.Nx = N[0];
+  P.Ny = N[1];
+  P.Nz = N[2];
+  P.zoff = s->zoff(field);
+  P.d = s->d;
+  P.n1 = s->n1;
+  P.h = s->h;
+  P.amp = amp;
+  for (int ax = 0; ax < 3; ++ax) {
+    P.x0[ax] = s->x_min[ax] + (field == 0 ? 0.0 : 0.5 * s->h);
+    P.w[ax] = ax < s->d ? w[ax] : 0.0;
+    P.phase[ax] = ax < s->d ? phase[ax] : 0.0;
+  }
+  s->launches += hlfk::launch_fill(P, s->stream);
+  HLF_CUDA(s, cudaGetLastError());
+  return HLF_OK;
+}
+
+hlf_status hlf_zero_field(hlf_solver* s, int field) {
+  if (!s || !valid_field(s, field)) return fail(s, HLF_INVALID_ARGUMENT, "bad field");
+  cudaSetDevice(s->device);
+  const size_t bytes = static_cast<size_t>(s->layers[field]) * s->layer_stride(field) * sizeof(double);
+  HLF_CUDA(s, cudaMemsetAsync(s->field[field], 0, bytes, s->stream));
+  return HLF_OK;
+}
+
+hlf_status hlf_halo_send_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr, int64_t* count) {
+  if (!s || s->d != 3 || (kind == 1 && (comp < 0 || comp > 2)))
+    return fail(s, HLF_INVALID_ARGUMENT, "halos exist for d = 3 only");
+  const int Kz = s->K[2];
+  if (kind == 0) {
+    *dev_ptr = s->field[0];  // p layer 0 -> previous rank's layer Kz
+    *count = s->layer_stride(0);
+  } else {
+    *dev_ptr = s->field[1 + comp] + Kz * s->layer_stride(1 + comp);  // v layer Kz-1 -> next rank's ghost
+    *count = s->layer_stride(1 + comp);
+  }
+  return HLF_OK;
+}
+
+hlf_status hlf_halo_recv_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr, int64_t* count) {
+  if (!s || s->d != 3 || (kind == 1 && (comp < 0 || comp > 2)))
+    return fail(s, HLF_INVALID_ARGUMENT, "halos exist for d = 3 only");
+  const int Kz = s->K[2];
+  if (kind == 0) {
+    *dev_ptr = s->field[0] + Kz * s->layer_stride(0);
+    *count = s->layer_stride(0);
+  } else {
+    *dev_ptr = s->field[1 + comp];
+    *count = s->layer_stride(1 + comp);
+  }
+  return HLF_OK;
+}
+
+int64_t hlf_launch_count(const hlf_solver* s) { return s ? s->launches : -1; }
+int hlf_kernel_variant(const hlf_solver* s) { return s ? s->variant : -1; }
+
+hlf_status hlf_set_kernel_variant(hlf_solver* s, int variant) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (variant == 1 && !(s->d == 3 && !s->variable && hlfk::tiled3d_supported(s->m)))
+    return fail(s, HLF_CONFIG_ERROR, "tiled 3D kernel not available for this configuration");
+  if (variant != 0 && variant != 1) return fail(s, HLF_INVALID_ARGUMENT, "unknown variant");
+  s->variant = variant;
+  return HLF_OK;
+}
+
+}  // extern "C"

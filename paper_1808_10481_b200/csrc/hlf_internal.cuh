@@ -1,0 +1,74 @@
+// Internal declarations shared by the host orchestration (hlf_capi.cu) and the
+// kernels.  Everything is FP64; the method is arXiv 1808.10481's
+// Hermite-leapfrog scheme (reference: /root/reference/proj, 1D only; the d-dim
+// generalization follows SURVEY.md App. A.3).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hlfk {
+
+constexpr int kMaxM = 8;                 // SchemeConfig::m_cap (config.hpp:31)
+constexpr int kMaxN = 2 * kMaxM + 2;     // 2m+2
+
+// Which staggered half step a launch performs.
+//   VEL: target = dual nodes (velocity), source = p at the 2^d primary corners
+//        (Stepper1d::advance_v, stepper1d.cpp:158-166)
+//   PRE: target = primary nodes (pressure), source = v at the 2^d dual corners
+//        (Stepper1d::advance_p, stepper1d.cpp:147-156)
+enum HalfKind { VEL = 0, PRE = 1 };
+
+// Kernel parameters, passed by value (lives in the constant parameter bank, so
+// M and the CK weights are free DFMA operands).
+struct HalfParams {
+  double M[kMaxN * kMaxN];      // interpolation operator, row-major (interpolation.cpp:42-44)
+  // Closed-form CK weights for constant coefficients:
+  //   G[k] = w_{2k+1} / h^{2k+1} * (VEL: av^{k+1} ap^k | PRE: ap^{k+1} av^k)
+  // with w_r = 2 prod_{q<=r} (dt/2)/q (leapfrog_half_update, stepper1d.cpp:54-61)
+  double G[kMaxM + 1];
+  double w[kMaxN];              // w_r for the iterated (variable-coefficient) form
+  double inv_h;
+  double ap, av;
+  const double* src[3];         // source field bases (layer 0 of the allocation)
+  double* dst[3];               // target field bases
+  const double* coeff;          // per-target-node ap jets [z][E][y][x] or null
+  int64_t s_layer, s_coef;      // source strides (elements)
+  int64_t t_layer, t_coef;      // target strides
+  int64_t c_layer, c_coef;      // coefficient-jet strides
+  int sNx, sNy;                 // source plane size
+  int tNx, tNy, tNz;            // target nodes to update
+  int t_zoff;                   // layer index of target z = 0 (p: 0, v: 1)
+  int s_zoff;                   // layer index of source z = 0
+  int K[3];
+  int bnd[3];                   // 0 periodic, 1 reflective (x, y in-kernel; z via ghost layers)
+  int step;                     // step index for the finite flag, -1 = do not record
+  int* flag;                    // first non-finite step (atomicMin)
+};
+
+struct FillParams {
+  double* dst;
+  int64_t layer, coef;
+  int Nx, Ny, Nz, zoff;
+  int d, n1;
+  double x0[3];                 // coordinate of node 0 along each axis
+  double h, amp;
+  double w[3], phase[3];
+};
+
+// launchers (return the number of kernels launched)
+int launch_half_generic(int d, int m, bool variable, HalfKind kind, const HalfParams& p,
+                        cudaStream_t st);
+int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
+bool tiled3d_supported(int m);
+int launch_fill(const FillParams& p, cudaStream_t st);
+// z ghost mirror for the dual family: dst layer = sign * (-1)^{c_z} src layer
+int launch_mirror_layer(double* dst, const double* src, int64_t plane, int n1, int d, double sigma,
+                        cudaStream_t st);
+// AoS [node][coef] chunk <-> SoA field (x-major node order)
+int launch_aos_to_soa(const double* aos, double* field, int64_t node0, int64_t count, int F,
+                      int Nx, int Ny, int Nz, int64_t layer, int64_t coef, int zoff, cudaStream_t st);
+int launch_soa_to_aos(const double* field, double* aos, int64_t node0, int64_t count, int F,
+                      int Nx, int Ny, int Nz, int64_t layer, int64_t coef, int zoff, cudaStream_t st);
+
+}  // namespace hlfk

@@ -1,0 +1,357 @@
+// Generic Hermite-leapfrog half-step kernels, any d in {1,2,3} and order m
+// (d<=2: m<=8; d=3: m<=4).  One thread per target node; the stacked corner
+// tensor and the reconstruction live in thread-local arrays.  This is the
+// correctness path for every configuration and the production path for 1D;
+// the 3D headline runs the tiled kernel in kernels_tiled3d.cu.
+//
+// Per target node:
+//   1. gather the (m+1)^d jets of the 2^d source corners into the stacked
+//      n^d tensor, index side*(m+1)+l per axis (reconstruct_cell_1d/2d,
+//      interpolation.cpp:63-113), mirroring ghosts across reflective walls;
+//   2. apply M along x, then y, then z (interpolation.cpp:87-112);
+//   3. constant coefficients: closed-form odd CK terms
+//        v_c[o] += sum_k G_k sum_{|b|=k} k!/b! prod (o+a)!/o! P[o+a], a = 2b + e_c
+//        p[o]   += sum_k G_k sum_{|b|=k} k!/b! prod (o+2b)!/o! W[o+2b],
+//                  W[q] = sum_c (q_c+1) V_c[q+e_c]
+//      variable ap jets: the iterated, truncated recurrence of
+//      ck_recurrence_variable (stepper1d.cpp:22-38) with tensor products
+//      (jet.cpp:109-121) and the leapfrog sum of leapfrog_half_update
+//      (stepper1d.cpp:54-61);
+//   4. in-place update of the target jet and the non-finite flag
+//      (check_finite, stepper1d.cpp:121-129).
+#include "hlf_internal.cuh"
+
+namespace hlfk {
+namespace {
+
+__host__ __device__ constexpr int cpow(int b, int e) { return e == 0 ? 1 : b * cpow(b, e - 1); }
+
+__device__ __forceinline__ double ffac(int o, int j) {
+  // (o+j)!/o!, exact in double for the ranges used here
+  double r = 1.0;
+  for (int t = 1; t <= j; ++t) r *= static_cast<double>(o + t);
+  return r;
+}
+
+__device__ __forceinline__ double fact(int k) {
+  double r = 1.0;
+  for (int t = 2; t <= k; ++t) r *= t;
+  return r;
+}
+
+template <int D>
+struct Idx {
+  // tensor of extent N per axis, x-major: e = sum_ax q_ax N^(D-1-ax)
+  template <int N>
+  __device__ static __forceinline__ int flat(const int* q) {
+    int e = 0;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) e = e * N + q[ax];
+    return e;
+  }
+  template <int N>
+  __device__ static __forceinline__ void split(int e, int* q) {
+#pragma unroll
+    for (int ax = D - 1; ax >= 0; --ax) {
+      q[ax] = e % N;
+      e /= N;
+    }
+  }
+};
+
+template <int D, int MM, bool VAR, int KIND>
+__global__ void __launch_bounds__(128) half_generic(const __grid_constant__ HalfParams P) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  constexpr int F = cpow(n1, D), E = cpow(n, D);
+  constexpr int NSRC = KIND == VEL ? 1 : D;
+
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = static_cast<int64_t>(P.tNx) * P.tNy * P.tNz;
+  if (tid >= total) return;
+  int t[3];
+  t[0] = static_cast<int>(tid % P.tNx);
+  const int64_t rest = tid / P.tNx;
+  t[1] = static_cast<int>(rest % P.tNy);
+  t[2] = static_cast<int>(rest / P.tNy);
+
+  // ---- corner addresses (plane offset + layer) and reflection flags ----
+  // axes 0..min(D,2)-1 are in-plane (x, y); axis 2 (z, d = 3) uses layers
+  int64_t coff[1 << D];
+  int cflip[1 << D];  // bit ax set: mirrored across a wall normal to ax
+#pragma unroll
+  for (int corner = 0; corner < (1 << D); ++corner) {
+    int s[3] = {0, 0, 0};
+    int flip = 0;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+      const int side = (corner >> ax) & 1;
+      int q = KIND == VEL ? t[ax] + side : t[ax] - 1 + side;
+      if (ax < 2) {
+        if (P.bnd[ax] == 0) {
+          if (q >= P.K[ax]) q -= P.K[ax];
+          if (q < 0) q += P.K[ax];
+        } else if (KIND == PRE) {
+          if (q < 0) {
+            q = 0;
+            flip |= 1 << ax;
+          } else if (q >= P.K[ax]) {
+            q = P.K[ax] - 1;
+            flip |= 1 << ax;
+          }
+        }
+      }
+      s[ax] = q;
+    }
+    const int layer = D == 3 ? P.s_zoff + s[2] : 0;
+    coff[corner] = static_cast<int64_t>(layer) * P.s_layer + static_cast<int64_t>(D >= 2 ? s[1] : 0) * P.sNx + s[0];
+    cflip[corner] = flip;
+  }
+
+  const int64_t toff = static_cast<int64_t>(D == 3 ? P.t_zoff + t[2] : 0) * P.t_layer +
+                       static_cast<int64_t>(D >= 2 ? t[1] : 0) * P.tNx + t[0];
+
+  double S[E];
+  double W[KIND == PRE ? E : 1];
+  if (KIND == PRE) {
+#pragma unroll 1
+    for (int e = 0; e < E; ++e) W[e] = 0.0;
+  }
+  // variable-coefficient tables: P (E) and V_c (D*E)
+  double Pt[VAR ? E : 1];
+  double Vt[VAR ? D * E : 1];
+
+  bool bad = false;
+
+#pragma unroll 1
+  for (int comp = 0; comp < NSRC; ++comp) {
+    const double* src = P.src[comp];
+    // 1. stacked corners
+#pragma unroll 1
+    for (int corner = 0; corner < (1 << D); ++corner) {
+#pragma unroll 1
+      for (int f = 0; f < F; ++f) {
+        int a[3];
+        Idx<D>::template split<n1>(f, a);
+        double sign = 1.0;
+        int q[3];
+#pragma unroll
+        for (int ax = 0; ax < D; ++ax) {
+          if ((cflip[corner] >> ax) & 1) {
+            if (a[ax] & 1) sign = -sign;
+            if (comp != ax) sign = -sign;  // tangential velocity is odd across the wall
+          }
+          q[ax] = ((corner >> ax) & 1) * n1 + a[ax];
+        }
+        S[Idx<D>::template flat<n>(q)] = sign * __ldg(src + coff[corner] + f * P.s_coef);
+      }
+    }
+    // 2. tensor sweeps, x first (interpolation.cpp:87-112)
+#pragma unroll 1
+    for (int ax = 0; ax < D; ++ax) {
+      const int stride = cpow(n, D - 1 - ax);
+#pragma unroll 1
+      for (int e = 0; e < E; ++e) {
+        if ((e / stride) % n != 0) continue;
+        double in[n];
+#pragma unroll
+        for (int s = 0; s < n; ++s) in[s] = S[e + s * stride];
+#pragma unroll
+        for (int r = 0; r < n; ++r) {
+          double acc = 0.0;
+#pragma unroll
+          for (int s = 0; s < n; ++s) acc = fma(P.M[r * n + s], in[s], acc);
+          S[e + r * stride] = acc;
+        }
+      }
+    }
+    if (VAR) {
+      if (KIND == PRE) {
+#pragma unroll 1
+        for (int e = 0; e < E; ++e) Vt[comp * E + e] = S[e];
+      } else {
+#pragma unroll 1
+        for (int e = 0; e < E; ++e) Pt[e] = S[e];
+      }
+    } else if (KIND == PRE) {
+      // W[q] += (q_c+1) V_c[q+e_c]
+      const int stride = cpow(n, D - 1 - comp);
+#pragma unroll 1
+      for (int e = 0; e < E; ++e) {
+        const int qc = (e / stride) % n;
+        if (qc + 1 < n) W[e] += static_cast<double>(qc + 1) * S[e + stride];
+      }
+    }
+  }
+
+  if (!VAR) {
+    // 3. closed-form odd CK sum (constant coefficients)
+    constexpr int NOUT = KIND == VEL ? D : 1;
+#pragma unroll 1
+    for (int c = 0; c < NOUT; ++c) {
+      double* dst = P.dst[c];
+#pragma unroll 1
+      for (int f = 0; f < F; ++f) {
+        int o[3] = {0, 0, 0};
+        Idx<D>::template split<n1>(f, o);
+        double acc = 0.0;
+#pragma unroll 1
+        for (int k = 0; k <= MM; ++k) {
+          double kpart = 0.0;
+          const double kf = fact(k);
+#pragma unroll 1
+          for (int b0 = 0; b0 <= k; ++b0) {
+#pragma unroll 1
+            for (int b1 = 0; b1 <= (D >= 2 ? k - b0 : 0); ++b1) {
+              const int b2 = D == 3 ? k - b0 - b1 : 0;
+              if (D == 1 && b0 != k) continue;
+              if (D == 2 && b0 + b1 != k) continue;
+              const int b[3] = {b0, b1, b2};
+              int q[3];
+              double coef = kf;
+              bool ok = true;
+#pragma unroll
+              for (int ax = 0; ax < D; ++ax) {
+                const int add = 2 * b[ax] + ((KIND == VEL && ax == c) ? 1 : 0);
+                q[ax] = o[ax] + add;
+                if (q[ax] >= n) ok = false;
+                coef *= ffac(o[ax], add) / fact(b[ax]);
+              }
+              if (!ok) continue;
+              const double val = KIND == VEL ? S[Idx<D>::template flat<n>(q)]
+                                             : W[Idx<D>::template flat<n>(q)];
+              kpart = fma(coef, val, kpart);
+            }
+          }
+          acc = fma(P.G[k], kpart, acc);
+        }
+        double* ptr = dst + toff + f * P.t_coef;
+        const double nv = *ptr + acc;
+        bad |= !isfinite(nv);
+        *ptr = nv;
+      }
+    }
+  } else {
+    // 3'. iterated truncated recurrence with per-node ap jets and scalar av
+    const double* apj = P.coeff + static_cast<int64_t>(D == 3 ? t[2] : 0) * P.c_layer +
+                        static_cast<int64_t>(D >= 2 ? t[1] : 0) * P.tNx + t[0];
+    double acc_out[KIND == VEL ? D * F : F];
+#pragma unroll 1
+    for (int i = 0; i < (KIND == VEL ? D * F : F); ++i) acc_out[i] = 0.0;
+    double tmp[E];
+#pragma unroll 1
+    for (int r = 0; r + 1 < n; ++r) {
+      // which table is non-zero at level r: VEL seeds P (even r -> P), PRE seeds V
+      const bool p_live = (KIND == VEL) == (r % 2 == 0);
+      if (p_live) {
+        // V_c[r+1] = av d_c P[r]
+#pragma unroll 1
+        for (int c = 0; c < D; ++c) {
+          const int stride = cpow(n, D - 1 - c);
+#pragma unroll 1
+          for (int e = 0; e < E; ++e) {
+            const int qc = (e / stride) % n;
+            Vt[c * E + e] = qc + 1 < n ? P.av * (Pt[e + stride] * (qc + 1) * P.inv_h) : 0.0;
+          }
+        }
+        if (KIND == VEL && ((r + 1) & 1)) {
+#pragma unroll 1
+          for (int c = 0; c < D; ++c)
+#pragma unroll 1
+            for (int f = 0; f < F; ++f) {
+              int o[3] = {0, 0, 0};
+              Idx<D>::template split<n1>(f, o);
+              acc_out[c * F + f] = fma(P.w[r + 1], Vt[c * E + Idx<D>::template flat<n>(o)], acc_out[c * F + f]);
+            }
+        }
+      } else {
+        // P[r+1] = ap (.) sum_c d_c V_c[r]
+#pragma unroll 1
+        for (int e = 0; e < E; ++e) tmp[e] = 0.0;
+#pragma unroll 1
+        for (int c = 0; c < D; ++c) {
+          const int stride = cpow(n, D - 1 - c);
+#pragma unroll 1
+          for (int e = 0; e < E; ++e) {
+            const int qc = (e / stride) % n;
+            if (qc + 1 < n) tmp[e] += Vt[c * E + e + stride] * (qc + 1) * P.inv_h;
+          }
+        }
+        // truncated tensor product (jet.cpp:109-121)
+#pragma unroll 1
+        for (int e = 0; e < E; ++e) {
+          int q[3] = {0, 0, 0};
+          Idx<D>::template split<n>(e, q);
+          double s = 0.0;
+#pragma unroll 1
+          for (int ei = 0; ei < E; ++ei) {
+            int qi[3] = {0, 0, 0};
+            Idx<D>::template split<n>(ei, qi);
+            bool ok = true;
+            int qr[3] = {0, 0, 0};
+#pragma unroll
+            for (int ax = 0; ax < D; ++ax) {
+              qr[ax] = q[ax] - qi[ax];
+              if (qr[ax] < 0) ok = false;
+            }
+            if (!ok) continue;
+            s = fma(__ldg(apj + ei * P.c_coef), tmp[Idx<D>::template flat<n>(qr)], s);
+          }
+          Pt[e] = s;
+        }
+        if (KIND == PRE && ((r + 1) & 1)) {
+#pragma unroll 1
+          for (int f = 0; f < F; ++f) {
+            int o[3] = {0, 0, 0};
+            Idx<D>::template split<n1>(f, o);
+            acc_out[f] = fma(P.w[r + 1], Pt[Idx<D>::template flat<n>(o)], acc_out[f]);
+          }
+        }
+      }
+    }
+    constexpr int NOUT = KIND == VEL ? D : 1;
+#pragma unroll 1
+    for (int c = 0; c < NOUT; ++c)
+#pragma unroll 1
+      for (int f = 0; f < F; ++f) {
+        double* ptr = P.dst[c] + toff + f * P.t_coef;
+        const double nv = *ptr + acc_out[c * F + f];
+        bad |= !isfinite(nv);
+        *ptr = nv;
+      }
+  }
+
+  if (bad && P.step >= 0) atomicMin(P.flag, P.step);
+}
+
+template <int D, int MM>
+int launch_dm(bool variable, HalfKind kind, const HalfParams& p, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(p.tNx) * p.tNy * p.tNz;
+  const int threads = 128;
+  const unsigned blocks = static_cast<unsigned>((total + threads - 1) / threads);
+  if (blocks == 0) return 0;
+  if (kind == VEL) {
+    if (variable) half_generic<D, MM, true, VEL><<<blocks, threads, 0, st>>>(p);
+    else half_generic<D, MM, false, VEL><<<blocks, threads, 0, st>>>(p);
+  } else {
+    if (variable) half_generic<D, MM, true, PRE><<<blocks, threads, 0, st>>>(p);
+    else half_generic<D, MM, false, PRE><<<blocks, threads, 0, st>>>(p);
+  }
+  return 1;
+}
+
+}  // namespace
+
+int launch_half_generic(int d, int m, bool variable, HalfKind kind, const HalfParams& p,
+                        cudaStream_t st) {
+#define HLF_CASE(D, MM) \
+  if (d == D && m == MM) return launch_dm<D, MM>(variable, kind, p, st);
+  HLF_CASE(1, 0) HLF_CASE(1, 1) HLF_CASE(1, 2) HLF_CASE(1, 3) HLF_CASE(1, 4)
+  HLF_CASE(1, 5) HLF_CASE(1, 6) HLF_CASE(1, 7) HLF_CASE(1, 8)
+  HLF_CASE(2, 0) HLF_CASE(2, 1) HLF_CASE(2, 2) HLF_CASE(2, 3) HLF_CASE(2, 4)
+  HLF_CASE(2, 5) HLF_CASE(2, 6) HLF_CASE(2, 7) HLF_CASE(2, 8)
+  HLF_CASE(3, 0) HLF_CASE(3, 1) HLF_CASE(3, 2) HLF_CASE(3, 3) HLF_CASE(3, 4)
+#undef HLF_CASE
+  return -1;
+}
+
+}  // namespace hlfk

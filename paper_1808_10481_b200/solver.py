@@ -1,0 +1,378 @@
+"""Host-side mirror of the reference's solver interface (proj/include/hlf) over
+the C-ABI of lib/libhlf_b200.so.
+
+Names, argument meaning and error behaviour follow the reference:
+  ConfigError / InstabilityError(step)         config.hpp:15-24
+  SchemeConfig.validate / dt_nominal_1d/_2d    config.hpp:30-44, config.cpp:27-32
+  step_count(T, dt)                            config.cpp:34-38
+  Grid1d.over / Grid2d.over                    grid.hpp:7-39, grid.cpp:9-33
+  build_interp_operator(m) -> InterpOperator   interpolation.hpp:14-22
+  Stepper.advance_p / advance_v / step_system  stepper1d.hpp:72-74
+The staggered state lives on the device inside the Stepper (the reference's
+caller-owned State1d, stepper1d.hpp:49-52, becomes set_field/get_field plus the
+t_p/t_v/dt properties).  Every compute call runs the sm_100a kernels; nothing
+here computes a half step on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib as _L
+
+PERIODIC = 0
+REFLECTIVE = 1
+PRIMARY = 0
+DUAL = 1
+
+
+class ConfigError(RuntimeError):
+    """hlf::ConfigError (config.hpp:15-17)."""
+
+
+class InstabilityError(RuntimeError):
+    """hlf::InstabilityError (config.hpp:19-24): carries the step index."""
+
+    def __init__(self, step: int, what: str):
+        super().__init__(what)
+        self.step = step
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _check(status: int, handle=None):
+    if status == _L.HLF_OK:
+        return
+    msg = _L.lib().hlf_last_error(handle)
+    msg = msg.decode() if msg else ""
+    if status == _L.HLF_CONFIG_ERROR:
+        raise ConfigError(msg)
+    if status == _L.HLF_INSTABILITY:
+        step = int(msg.rsplit(" ", 1)[-1]) if msg else -1
+        raise InstabilityError(step, msg)
+    if status == _L.HLF_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    raise CudaError(msg or f"status {status}")
+
+
+# ---------------------------------------------------------------- config
+
+
+def step_count(T: float, dt_nominal: float) -> int:
+    """n = ceil(T / dt_nominal) (config.cpp:34-38)."""
+    if not T > 0.0:
+        raise ConfigError("final time must be positive")
+    if not dt_nominal > 0.0:
+        raise ConfigError("nominal dt must be positive")
+    return int(math.ceil(T / dt_nominal))
+
+
+@dataclass
+class SchemeConfig:
+    """hlf::SchemeConfig (config.hpp:30-44); dt_nominal_3d extends the 2D rule
+    with 1/sqrt(3)."""
+
+    m: int = 2
+    cfl: float = 0.9
+    m_cap: int = 8
+
+    def validate(self):
+        if self.m < 0 or self.m > self.m_cap:
+            raise ConfigError(f"scheme order m must be in [0, {self.m_cap}]")
+        if not (self.cfl > 0.0) or not math.isfinite(self.cfl):
+            raise ConfigError("cfl must be positive and finite")
+
+    def dt_nominal_1d(self, h: float, c_max: float) -> float:
+        return self.cfl * h / c_max
+
+    def dt_nominal_2d(self, h: float, c_max: float) -> float:
+        return self.cfl * h / math.sqrt(2.0) / c_max
+
+    def dt_nominal_3d(self, h: float, c_max: float) -> float:
+        return self.cfl * h / math.sqrt(3.0) / c_max
+
+    def dt_nominal(self, dim: int, h: float, c_max: float) -> float:
+        return (self.dt_nominal_1d, self.dt_nominal_2d, self.dt_nominal_3d)[dim - 1](h, c_max)
+
+
+@dataclass
+class Grid:
+    """Uniform grid with a common spacing (Grid1d/Grid2d, grid.hpp:7-39)."""
+
+    x_min: tuple
+    h: float
+    K: tuple
+
+    @property
+    def dim(self) -> int:
+        return len(self.K)
+
+    @staticmethod
+    def over(lo: Sequence[float], hi: Sequence[float], K) -> "Grid":
+        lo = list(lo)
+        hi = list(hi)
+        Ks = list(K) if hasattr(K, "__len__") else [K] * len(lo)
+        for k in Ks:
+            if k < 2:
+                raise ConfigError("grid needs K >= 2")
+        hs = []
+        for a, b, k in zip(lo, hi, Ks):
+            if not b > a:
+                raise ConfigError("grid needs a nonempty box")
+            hs.append((b - a) / k)
+        for x in hs[1:]:
+            if abs(x - hs[0]) > 1e-12 * abs(hs[0]):
+                raise ConfigError("grid must be square (equal spacing in x and y)")
+        return Grid(tuple(lo), hs[0], tuple(Ks))
+
+    def primary(self, ax: int, i: int) -> float:
+        return self.x_min[ax] + i * self.h
+
+    def dual(self, ax: int, i: int) -> float:
+        return self.x_min[ax] + (i + 0.5) * self.h
+
+
+class Grid1d(Grid):
+    @staticmethod
+    def over(x_min: float, x_max: float, K: int) -> Grid:  # grid.cpp:9-17
+        return Grid.over([x_min], [x_max], [K])
+
+
+class Grid2d(Grid):
+    @staticmethod
+    def over(x_min, x_max, y_min, y_max, K: int) -> Grid:  # grid.cpp:19-33
+        return Grid.over([x_min, y_min], [x_max, y_max], [K, K])
+
+
+class Grid3d(Grid):
+    @staticmethod
+    def over(x_min, x_max, y_min, y_max, z_min, z_max, K) -> Grid:
+        return Grid.over([x_min, y_min, z_min], [x_max, y_max, z_max], K)
+
+
+@dataclass
+class InterpOperator:
+    """hlf::InterpOperator (interpolation.hpp:14-19)."""
+
+    m: int
+    n: int
+    M: np.ndarray = field(repr=False)
+    condition: float = 0.0
+
+
+def build_interp_operator(m: int) -> InterpOperator:
+    n = 2 * m + 2
+    M = np.zeros(n * n if 0 <= m <= 8 else 1)
+    cond = C.c_double(0.0)
+    _check(_L.lib().hlf_build_interp_operator(m, M.ctypes.data_as(C.POINTER(C.c_double)), C.byref(cond)))
+    return InterpOperator(m, n, M.reshape(n, n), cond.value)
+
+
+# ---------------------------------------------------------------- stepper
+
+
+class Stepper:
+    """Hermite-leapfrog stepper on the B200 for d = 1, 2, 3.
+
+    Fields: 0 = p (primary grid), 1..d = velocity components (dual grid).
+    Host arrays are [node][coef], both x-major (see include/hlf_b200.h)."""
+
+    def __init__(self, grid: Grid, m: int, boundary=None, ap: float = -1.0, av: float = -1.0,
+                 variable_ap: bool = False, M: np.ndarray | None = None, device: int = 0,
+                 stream: int | None = None, z_slab: bool = False):
+        SchemeConfig(m=m).validate()  # Stepper1d ctor guard (stepper1d.cpp:95-98)
+        L = _L.lib()
+        d = grid.dim
+        boundary = list(boundary) if boundary is not None else [PERIODIC] * d
+        desc = _L.HlfDesc()
+        desc.dim = d
+        desc.m = m
+        for ax in range(3):
+            desc.K[ax] = grid.K[ax] if ax < d else 1
+            desc.x_min[ax] = grid.x_min[ax] if ax < d else 0.0
+            desc.boundary[ax] = boundary[ax] if ax < d else PERIODIC
+        desc.h = grid.h
+        desc.ap = ap
+        desc.av = av
+        desc.variable_ap = int(variable_ap)
+        self.op = build_interp_operator(m)
+        self._M = np.ascontiguousarray(M if M is not None else self.op.M, dtype=np.float64).ravel()
+        desc.M = self._M.ctypes.data_as(C.POINTER(C.c_double))
+        desc.device = device
+        desc.stream = stream
+        desc.z_slab = int(z_slab)
+        h = C.c_void_p()
+        _check(L.hlf_create(C.byref(desc), C.byref(h)), None)
+        self._h = h
+        self._L = L
+        self.grid, self.m, self.dim = grid, m, d
+        self.boundary = boundary
+        self.ap, self.av = ap, av
+        self.n1, self.n = m + 1, 2 * m + 2
+        self.F = self.n1 ** d
+        self.E = self.n ** d
+        self.device = device
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.hlf_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, status):
+        _check(status, self._h)
+
+    # -- geometry
+    def num_nodes(self, grid: int) -> int:
+        return int(self._L.hlf_num_nodes(self._h, grid))
+
+    def field_nodes(self, f: int) -> int:
+        return self.num_nodes(PRIMARY if f == 0 else DUAL)
+
+    def node_shape(self, f: int) -> tuple:
+        K = self.grid.K
+        if f == 0:
+            return tuple(k + 1 if b == REFLECTIVE else k for k, b in zip(K, self.boundary))
+        return tuple(K)
+
+    # -- state
+    def set_field(self, f: int, host: np.ndarray):
+        a = np.ascontiguousarray(host, dtype=np.float64)
+        if a.size != self.field_nodes(f) * self.F:
+            raise ValueError("field buffer has the wrong size")
+        self._c(self._L.hlf_set_field(self._h, f, a.ctypes.data))
+
+    def set_field_ptr(self, f: int, host_ptr: int):
+        """Upload from a host pointer (e.g. pinned torch memory) of the right size."""
+        self._c(self._L.hlf_set_field(self._h, f, host_ptr))
+
+    def get_field(self, f: int, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.field_nodes(f), self.F), dtype=np.float64)
+        self._c(self._L.hlf_get_field(self._h, f, out.ctypes.data))
+        return out
+
+    def get_field_ptr(self, f: int, host_ptr: int):
+        self._c(self._L.hlf_get_field(self._h, f, host_ptr))
+
+    def set_coeff(self, grid: int, jets: np.ndarray):
+        a = np.ascontiguousarray(jets, dtype=np.float64)
+        if a.size != self.num_nodes(grid) * self.E:
+            raise ValueError("coefficient buffer has the wrong size")
+        self._c(self._L.hlf_set_coeff(self._h, grid, a.ctypes.data))
+
+    def set_times(self, t_p: float, t_v: float, dt: float):
+        self._c(self._L.hlf_set_times(self._h, t_p, t_v, dt))
+
+    def times(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        self._c(self._L.hlf_get_times(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    @property
+    def t_p(self):
+        return self.times()[0]
+
+    @property
+    def t_v(self):
+        return self.times()[1]
+
+    @property
+    def dt(self):
+        return self.times()[2]
+
+    @dt.setter
+    def dt(self, value: float):
+        self._c(self._L.hlf_set_dt(self._h, value))
+
+    # -- stepping
+    def advance_p(self):
+        self._c(self._L.hlf_advance_p(self._h))
+
+    def advance_v(self):
+        self._c(self._L.hlf_advance_v(self._h))
+
+    def step_system(self, step_index: int):
+        self._c(self._L.hlf_step(self._h, step_index))
+
+    def advance_n(self, n: int, first_step: int = 0):
+        self._c(self._L.hlf_advance_n(self._h, n, first_step))
+
+    def advance_to(self, T: float, cfl: float = 0.9, c_max: float = 1.0, t0: float | None = None) -> int:
+        """Run to T with n = step_count(T, dt_nominal) steps of dt = T/n,
+        the caller loop of tests/test_stepper1d.cpp:29-38."""
+        cfg = SchemeConfig(m=self.m, cfl=cfl)
+        n = step_count(T, cfg.dt_nominal(self.dim, self.grid.h, c_max))
+        self.advance_n(n, 0)
+        return n
+
+    def poll_finite(self) -> int:
+        bad = C.c_int(-1)
+        self._c(self._L.hlf_poll_finite(self._h, C.byref(bad)))
+        return bad.value
+
+    def clear_finite(self):
+        self._c(self._L.hlf_clear_finite(self._h))
+
+    def synchronize(self):
+        self._c(self._L.hlf_synchronize(self._h))
+
+    # -- device data
+    def field_device(self, f: int):
+        ptr = C.c_void_p()
+        layer = C.c_int64()
+        coef = C.c_int64()
+        layers = C.c_int()
+        self._c(self._L.hlf_field_device(self._h, f, C.byref(ptr), C.byref(layer), C.byref(coef), C.byref(layers)))
+        return ptr.value, layer.value, coef.value, layers.value
+
+    def fill_separable(self, f: int, amp: float, w: Sequence[float], phase: Sequence[float]):
+        w3 = (C.c_double * 3)(*(list(w) + [0.0] * (3 - len(w))))
+        p3 = (C.c_double * 3)(*(list(phase) + [0.0] * (3 - len(phase))))
+        self._c(self._L.hlf_fill_separable(self._h, f, amp, w3, p3))
+
+    def zero_field(self, f: int):
+        self._c(self._L.hlf_zero_field(self._h, f))
+
+    def halo_ptr(self, kind: int, comp: int, send: bool):
+        ptr = C.c_void_p()
+        cnt = C.c_int64()
+        fn = self._L.hlf_halo_send_ptr if send else self._L.hlf_halo_recv_ptr
+        self._c(fn(self._h, kind, comp, C.byref(ptr), C.byref(cnt)))
+        return ptr.value, cnt.value
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._L.hlf_launch_count(self._h))
+
+    @property
+    def kernel_variant(self) -> int:
+        return int(self._L.hlf_kernel_variant(self._h))
+
+    @kernel_variant.setter
+    def kernel_variant(self, v: int):
+        self._c(self._L.hlf_set_kernel_variant(self._h, v))
+
+
+def Stepper1d(grid: Grid, m: int, **kw) -> Stepper:
+    return Stepper(grid, m, **kw)
+
+
+def Stepper2d(grid: Grid, m: int, **kw) -> Stepper:
+    return Stepper(grid, m, **kw)
+
+
+def Stepper3d(grid: Grid, m: int, **kw) -> Stepper:
+    return Stepper(grid, m, **kw)

@@ -1,0 +1,258 @@
+"""Parity of the sm_100a kernels (through the C-ABI) against the oracle.
+
+Bar (north star): ||gpu - cpu||_inf / ||cpu||_inf <= 1e-12 per field, FP64,
+identical inputs and step counts.  1D is also checked against the compiled
+reference's committed fixture (tests/golden/reference_1d.json)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1808_10481_b200 as H
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def rel_err(got, ref):
+    scale = np.abs(ref).max()
+    return np.abs(got - ref).max() / (scale if scale > 0 else 1.0)
+
+
+def make_pair(d, m, K, boundary=None, ap=-1.0, av=-1.0, variable=False, h=None, seed=0):
+    K = [K] * d if not hasattr(K, "__len__") else list(K)
+    boundary = boundary or [0] * d
+    h = h or 2.0 / K[0]
+    grid = H.Grid([-1.0] * d, h, tuple(K))
+    g = H.Stepper(grid, m, boundary=boundary, ap=ap, av=av, variable_ap=variable)
+    o = O.OracleStepper(d, m, K, h, boundary=boundary, ap=ap, av=av)
+    rng = np.random.default_rng(seed)
+    for f in range(d + 1):
+        n = g.field_nodes(f)
+        # decaying coefficients, like scaled jets of smooth data
+        scale = 0.6 ** np.arange(g.F)
+        a = rng.standard_normal((n, g.F)) * scale
+        g.set_field(f, a)
+        o.set_field(f, a)
+    return g, o
+
+
+def compare(g, o, d, tol=TOL):
+    errs = []
+    for f in range(d + 1):
+        e = rel_err(g.get_field(f), o.get_field(f))
+        errs.append(e)
+        assert e <= tol, (f, e)
+    assert g.times() == pytest.approx(o.get_times(), abs=0, rel=0)
+    return errs
+
+
+def run_both(g, o, steps, dt):
+    g.set_times(0.0, dt / 2, dt)
+    o.set_times(0.0, dt / 2, dt)
+    g.advance_n(steps)
+    assert o.advance_n(steps) == -1
+
+
+def test_config1_matches_reference_fixture(golden):
+    c1 = golden["config1"]
+    grid = H.Grid1d.over(-1.0, 1.0, c1["K"])
+    g = H.Stepper(grid, c1["m"])
+    g.set_field(0, np.array(c1["p0"]))
+    g.set_field(1, np.array(c1["v0"]))
+    g.set_times(*c1["times0"])
+    for i in range(c1["steps"]):
+        g.step_system(i)
+    assert g.times() == tuple(c1["times1"])
+    assert rel_err(g.get_field(0).ravel(), np.array(c1["p1"])) <= TOL
+    assert rel_err(g.get_field(1).ravel(), np.array(c1["v1"])) <= TOL
+
+
+def test_set_get_roundtrip_is_exact():
+    g, _ = make_pair(3, 2, [5, 6, 7], boundary=[1, 0, 1])
+    rng = np.random.default_rng(1)
+    for f in range(4):
+        a = rng.standard_normal((g.field_nodes(f), g.F))
+        g.set_field(f, a)
+        assert np.array_equal(g.get_field(f), a)
+
+
+@pytest.mark.parametrize("m", range(9))
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_parity_1d(m, boundary):
+    g, o = make_pair(1, m, 24, boundary=[boundary], seed=m)
+    run_both(g, o, 30, 0.4 * g.grid.h)
+    compare(g, o, 1)
+
+
+@pytest.mark.parametrize("m", range(5))
+@pytest.mark.parametrize("boundary", [[0, 0], [1, 1], [1, 0]])
+def test_parity_2d(m, boundary):
+    g, o = make_pair(2, m, [12, 10], boundary=boundary, seed=10 + m)
+    run_both(g, o, 8, 0.3 * g.grid.h)
+    compare(g, o, 2)
+
+
+@pytest.mark.parametrize("m", range(5))
+@pytest.mark.parametrize("boundary", [[0, 0, 0], [1, 1, 1], [0, 1, 0]])
+def test_parity_3d_generic(m, boundary):
+    K = [6, 5, 7] if m < 4 else [4, 4, 5]
+    g, o = make_pair(3, m, K, boundary=boundary, seed=20 + m)
+    g.kernel_variant = 0
+    run_both(g, o, 3, 0.25 * g.grid.h)
+    compare(g, o, 3)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_parity_3d_default_kernel(m):
+    g, o = make_pair(3, m, [16, 12, 10], seed=40 + m)
+    run_both(g, o, 3, 0.25 * g.grid.h)
+    compare(g, o, 3)
+
+
+def c2_jets(d, K, h, n, boundary, dual):
+    """ap = -c^2 with c^2 = 1 + sin(pi x) sin(pi y) / 2 (SURVEY.md sec. 8(d) cfg 3)."""
+    N = [k + 1 if (b == 1 and not dual) else k for k, b in zip(K, boundary)]
+    jets = np.zeros((int(np.prod(N)), n ** d))
+    O.add_separable(d, N, [-1.0] * d, h, 0.5 if dual else 0.0, n, 0.5, [math.pi] * d, [0.0] * d, jets)
+    jets[:, 0] += 1.0
+    return -jets
+
+
+@pytest.mark.parametrize("d,m,boundary", [(1, 3, [0]), (1, 2, [1]), (2, 1, [0, 0]), (2, 3, [1, 1]), (3, 1, [1, 1, 1])])
+def test_parity_variable_speed(d, m, boundary):
+    K = [10] * d if d < 3 else [5, 4, 6]
+    g, o = make_pair(d, m, K, boundary=boundary, variable=True, seed=60 + m)
+    n = 2 * m + 2
+    for grid, dual in ((0, False), (1, True)):
+        jets = c2_jets(d, K, g.grid.h, n, boundary, dual)
+        g.set_coeff(grid, jets)
+        o.set_coeff(grid, 0, jets)
+    run_both(g, o, 5, 0.2 * g.grid.h)
+    compare(g, o, d)
+
+
+def test_1d_variable_coefficients_vs_compiled_reference():
+    if not O.ref_available():
+        pytest.skip("compiled reference not present")
+    m, K = 3, 40
+    r = O.RefStepper1d("pv", m, K)
+    r.init_leapfrog(0.9 * r.h)
+    p0, v0, t0 = r.get()
+    g = H.Stepper(H.Grid1d.over(r.x_min, r.x_max, K), m, variable_ap=True, av=-1.0)
+    g.set_coeff(0, r.coeff(0, False))
+    g.set_coeff(1, r.coeff(0, True))
+    g.set_field(0, p0)
+    g.set_field(1, v0)
+    g.set_times(*t0)
+    g.advance_n(25)
+    assert r.steps(25) == -1
+    p1, v1, t1 = r.get()
+    assert rel_err(g.get_field(0), p1) <= TOL and rel_err(g.get_field(1), v1) <= TOL
+    assert g.times() == t1
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_time_reversal(d):
+    # tests/test_stepper1d.cpp:276-299, in d dimensions
+    m = 2
+    g, _ = make_pair(d, m, [10] * d if d < 3 else [8, 8, 8], seed=5)
+    p0 = g.get_field(0).copy()
+    v0 = [g.get_field(c).copy() for c in range(1, d + 1)]
+    dt = 0.07 * g.grid.h / 0.2
+    g.set_times(0.0, dt / 2, dt)
+    for i in range(20):
+        g.step_system(i)
+    g.dt = -dt
+    for _ in range(20):
+        g.advance_v()
+        g.advance_p()
+    assert rel_err(g.get_field(0), p0) <= 1e-11
+    for c in range(1, d + 1):
+        assert rel_err(g.get_field(c), v0[c - 1]) <= 1e-11
+    assert abs(g.t_p) <= 1e-12
+
+
+def test_linearity_3d():
+    # tests/test_stepper1d.cpp:242-274
+    m = 3
+    ga, _ = make_pair(3, m, [8, 8, 8], seed=1)
+    gb, _ = make_pair(3, m, [8, 8, 8], seed=2)
+    gab, _ = make_pair(3, m, [8, 8, 8], seed=3)
+    al, be = 0.6, -1.3
+    for f in range(4):
+        gab.set_field(f, al * ga.get_field(f) + be * gb.get_field(f))
+    for s in (ga, gb, gab):
+        s.set_times(0, 0.02, 0.04)
+        s.step_system(0)
+    for f in range(4):
+        ref = al * ga.get_field(f) + be * gb.get_field(f)
+        assert rel_err(gab.get_field(f), ref) <= 1e-12
+
+
+def test_zero_stays_zero():
+    g = H.Stepper(H.Grid([-1.0] * 3, 0.25, (8, 8, 8)), 3)
+    g.set_times(0, 0.05, 0.1)
+    g.advance_n(5)
+    for f in range(4):
+        assert np.abs(g.get_field(f)).max() == 0.0
+
+
+def test_instability_raises_with_step_index():
+    # tests/test_stepper1d.cpp:301-321: cfl 2.5 on the standing wave blows up
+    golden_grid = H.Grid1d.over(-1.0, 1.0, 16)
+    g = H.Stepper(golden_grid, 2)
+    o = O.OracleStepper(1, 2, [16], golden_grid.h)
+    p = np.zeros((16, 3))
+    v = np.zeros((16, 3))
+    O.add_separable(1, [16], [-1.0], golden_grid.h, 0.0, 3, 1.0, [2 * math.pi], [0.0], p)
+    g.set_field(0, p)
+    g.set_field(1, v)
+    o.set_field(0, p)
+    o.set_field(1, v)
+    dt = 2.5 * golden_grid.h
+    g.set_times(0, dt / 2, dt)
+    o.set_times(0, dt / 2, dt)
+    expected = o.advance_n(5000)
+    assert expected > 0
+    with pytest.raises(H.InstabilityError) as ei:
+        for i in range(5000):
+            g.step_system(i)
+    assert ei.value.step == expected
+    assert str(expected) in str(ei.value)
+    # advance_n reports the same first bad step
+    g2 = H.Stepper(golden_grid, 2)
+    g2.set_field(0, p)
+    g2.set_field(1, v)
+    g2.set_times(0, dt / 2, dt)
+    with pytest.raises(H.InstabilityError) as ei2:
+        g2.advance_n(expected + 10)
+    assert ei2.value.step == expected
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_fill_separable_matches_host_jets(d):
+    m = 3
+    K = [9, 7, 5][:d]
+    grid = H.Grid([-1.0] * d, 0.3, tuple(K))
+    g = H.Stepper(grid, m, boundary=[1] + [0] * (d - 1))
+    w = [1.3, -0.7, 2.1][:d]
+    ph = [0.2, 1.1, -0.4][:d]
+    for f, off in ((0, 0.0), (1, 0.5)):
+        g.fill_separable(f, 0.8, w, ph)
+        ref = np.zeros((g.field_nodes(f), g.F))
+        O.add_separable(d, list(g.node_shape(f)), [-1.0] * d, 0.3, off, m + 1, 0.8, w, ph, ref)
+        assert np.abs(g.get_field(f) - ref).max() <= 1e-14
+
+
+def test_advance_n_equals_step_loop():
+    ga, _ = make_pair(2, 3, [16, 16], seed=9)
+    gb, _ = make_pair(2, 3, [16, 16], seed=9)
+    for s in (ga, gb):
+        s.set_times(0, 0.01, 0.02)
+    ga.advance_n(7, 3)
+    for i in range(7):
+        gb.step_system(3 + i)
+    for f in range(3):
+        assert np.array_equal(ga.get_field(f), gb.get_field(f))

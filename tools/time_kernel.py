@@ -1,0 +1,30 @@
+"""Quick device timing of the half-step kernels (CUDA events via torch on the
+solver's stream). Usage: python tools/time_kernel.py d m K [steps] [variant]"""
+import sys, os, math, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_1808_10481_b200 as H
+
+d, m, K = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+steps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
+variant = int(sys.argv[5]) if len(sys.argv) > 5 else -1
+stream = torch.cuda.Stream()
+Ks = [K] * d
+g = H.Stepper(H.Grid([-1.0] * d, 2.0 / K, tuple(Ks)), m, stream=stream.cuda_stream)
+if variant >= 0:
+    g.kernel_variant = variant
+pi = math.pi
+g.fill_separable(0, 1.0, [pi] * d, [0.0] * d)
+for c in range(1, d + 1):
+    g.fill_separable(c, -0.1, [pi] * d, [pi / 2 if a == c - 1 else 0.0 for a in range(d)])
+dt = 0.9 * g.grid.h / math.sqrt(d)
+g.set_times(0, dt / 2, dt)
+g.advance_n(2)
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+e0.record(stream)
+g.advance_n(steps)
+e1.record(stream)
+e1.synchronize()
+ms = e0.elapsed_time(e1) / steps
+dof = (d + 1) * (m + 1) ** d * K ** d
+print(f"d={d} m={m} K={K} variant={g.kernel_variant} ms/step={ms:.3f} DOF/s={dof / ms * 1e3:.3e} GB/s(24B/DOF)={24 * dof / ms / 1e6:.1f}")
