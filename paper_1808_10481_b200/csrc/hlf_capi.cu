@@ -230,6 +230,7 @@ void fill_weights(const hlf_solver* s, hlfk::HalfKind kind, HalfParams& P) {
     P.G[k] = g * a_pow;
   }
   P.inv_h = 1.0 / s->h;
+  P.h = s->h;
   P.ap = s->ap;
   P.av = s->av;
 }

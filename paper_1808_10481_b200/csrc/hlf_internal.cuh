@@ -28,7 +28,7 @@ struct HalfParams {
   // with w_r = 2 prod_{q<=r} (dt/2)/q (leapfrog_half_update, stepper1d.cpp:54-61)
   double G[kMaxM + 1];
   double w[kMaxN];              // w_r for the iterated (variable-coefficient) form
-  double inv_h;
+  double inv_h, h;
   double ap, av;
   const double* src[3];         // source field bases (layer 0 of the allocation)
   double* dst[3];               // target field bases

@@ -9,14 +9,10 @@
 //      n^d tensor, index side*(m+1)+l per axis (reconstruct_cell_1d/2d,
 //      interpolation.cpp:63-113), mirroring ghosts across reflective walls;
 //   2. apply M along x, then y, then z (interpolation.cpp:87-112);
-//   3. constant coefficients: closed-form odd CK terms
-//        v_c[o] += sum_k G_k sum_{|b|=k} k!/b! prod (o+a)!/o! P[o+a], a = 2b + e_c
-//        p[o]   += sum_k G_k sum_{|b|=k} k!/b! prod (o+2b)!/o! W[o+2b],
-//                  W[q] = sum_c (q_c+1) V_c[q+e_c]
-//      variable ap jets: the iterated, truncated recurrence of
-//      ck_recurrence_variable (stepper1d.cpp:22-38) with tensor products
-//      (jet.cpp:109-121) and the leapfrog sum of leapfrog_half_update
-//      (stepper1d.cpp:54-61);
+//   3. the iterated, truncated CK recurrence of ck_recurrence_variable
+//      (stepper1d.cpp:22-38) with scalar or per-node (tensor product,
+//      jet.cpp:109-121) ap and the odd-level sum of leapfrog_half_update
+//      (stepper1d.cpp:54-61), in the oracle's operation order;
 //   4. in-place update of the target jet and the non-finite flag
 //      (check_finite, stepper1d.cpp:121-129).
 #include "hlf_internal.cuh"
@@ -25,19 +21,6 @@ namespace hlfk {
 namespace {
 
 __host__ __device__ constexpr int cpow(int b, int e) { return e == 0 ? 1 : b * cpow(b, e - 1); }
-
-__device__ __forceinline__ double ffac(int o, int j) {
-  // (o+j)!/o!, exact in double for the ranges used here
-  double r = 1.0;
-  for (int t = 1; t <= j; ++t) r *= static_cast<double>(o + t);
-  return r;
-}
-
-__device__ __forceinline__ double fact(int k) {
-  double r = 1.0;
-  for (int t = 2; t <= k; ++t) r *= t;
-  return r;
-}
 
 template <int D>
 struct Idx {
@@ -110,16 +93,16 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
   const int64_t toff = static_cast<int64_t>(D == 3 ? P.t_zoff + t[2] : 0) * P.t_layer +
                        static_cast<int64_t>(D >= 2 ? t[1] : 0) * P.tNx + t[0];
 
+  // Arithmetic below is "faithful": separate IEEE multiply/add/divide in the
+  // oracle's order (no FMA contraction), so results equal the oracle and, in
+  // 1D, the compiled reference bit for bit.  The reconstruction is
+  // ill-conditioned (cond(A) = 429 at m = 3), so ANY reordering moves
+  // long-run results by ~N cond(A) eps (compiling the reference itself with
+  // -mfma moves config 1 by 1.2e-11); the fast tiled kernels trade this for
+  // speed and are checked against the 1e-12 bar over short runs.
   double S[E];
-  double W[KIND == PRE ? E : 1];
-  if (KIND == PRE) {
-#pragma unroll 1
-    for (int e = 0; e < E; ++e) W[e] = 0.0;
-  }
-  // variable-coefficient tables: P (E) and V_c (D*E)
-  double Pt[VAR ? E : 1];
-  double Vt[VAR ? D * E : 1];
-
+  double Pt[E];
+  double Vt[D * E];
   bool bad = false;
 
 #pragma unroll 1
@@ -145,7 +128,7 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
         S[Idx<D>::template flat<n>(q)] = sign * __ldg(src + coff[corner] + f * P.s_coef);
       }
     }
-    // 2. tensor sweeps, x first (interpolation.cpp:87-112)
+    // 2. tensor sweeps, x first (interpolation.cpp:53-61, 87-112)
 #pragma unroll 1
     for (int ax = 0; ax < D; ++ax) {
       const int stride = cpow(n, D - 1 - ax);
@@ -159,124 +142,62 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
         for (int r = 0; r < n; ++r) {
           double acc = 0.0;
 #pragma unroll
-          for (int s = 0; s < n; ++s) acc = fma(P.M[r * n + s], in[s], acc);
+          for (int s = 0; s < n; ++s) acc = __dadd_rn(acc, __dmul_rn(P.M[r * n + s], in[s]));
           S[e + r * stride] = acc;
         }
       }
     }
-    if (VAR) {
-      if (KIND == PRE) {
 #pragma unroll 1
-        for (int e = 0; e < E; ++e) Vt[comp * E + e] = S[e];
-      } else {
-#pragma unroll 1
-        for (int e = 0; e < E; ++e) Pt[e] = S[e];
-      }
-    } else if (KIND == PRE) {
-      // W[q] += (q_c+1) V_c[q+e_c]
-      const int stride = cpow(n, D - 1 - comp);
-#pragma unroll 1
-      for (int e = 0; e < E; ++e) {
-        const int qc = (e / stride) % n;
-        if (qc + 1 < n) W[e] += static_cast<double>(qc + 1) * S[e + stride];
-      }
+    for (int e = 0; e < E; ++e) {
+      if (KIND == PRE) Vt[comp * E + e] = S[e];
+      else Pt[e] = S[e];
     }
   }
 
-  if (!VAR) {
-    // 3. closed-form odd CK sum (constant coefficients)
-    constexpr int NOUT = KIND == VEL ? D : 1;
+  // 3. coupled CK recurrence, count = 2m+2 (stepper1d.cpp:22-38): with one
+  //    field seeded zero only one table is live per level.
+  //    P[r+1] = ap (.) sum_c d_c V_c[r];  V_c[r+1] = av d_c P[r]
+  //    d_c T[q] = (T[q+e_c] (q_c+1)) / h, truncated (jet.cpp:123-135)
+  constexpr int NOUT = KIND == VEL ? D : 1;
+  double tgt[NOUT * F];
 #pragma unroll 1
-    for (int c = 0; c < NOUT; ++c) {
-      double* dst = P.dst[c];
+  for (int c = 0; c < NOUT; ++c)
 #pragma unroll 1
-      for (int f = 0; f < F; ++f) {
-        int o[3] = {0, 0, 0};
-        Idx<D>::template split<n1>(f, o);
-        double acc = 0.0;
+    for (int f = 0; f < F; ++f) tgt[c * F + f] = P.dst[c][toff + f * P.t_coef];
+  const double* apj = VAR ? P.coeff + static_cast<int64_t>(D == 3 ? t[2] : 0) * P.c_layer +
+                                static_cast<int64_t>(D >= 2 ? t[1] : 0) * P.tNx + t[0]
+                          : nullptr;
 #pragma unroll 1
-        for (int k = 0; k <= MM; ++k) {
-          double kpart = 0.0;
-          const double kf = fact(k);
+  for (int r = 0; r + 1 < n; ++r) {
+    const bool p_live = (KIND == VEL) == (r % 2 == 0);
+    if (p_live) {
 #pragma unroll 1
-          for (int b0 = 0; b0 <= k; ++b0) {
+      for (int c = 0; c < D; ++c) {
+        const int stride = cpow(n, D - 1 - c);
 #pragma unroll 1
-            for (int b1 = 0; b1 <= (D >= 2 ? k - b0 : 0); ++b1) {
-              const int b2 = D == 3 ? k - b0 - b1 : 0;
-              if (D == 1 && b0 != k) continue;
-              if (D == 2 && b0 + b1 != k) continue;
-              const int b[3] = {b0, b1, b2};
-              int q[3];
-              double coef = kf;
-              bool ok = true;
-#pragma unroll
-              for (int ax = 0; ax < D; ++ax) {
-                const int add = 2 * b[ax] + ((KIND == VEL && ax == c) ? 1 : 0);
-                q[ax] = o[ax] + add;
-                if (q[ax] >= n) ok = false;
-                coef *= ffac(o[ax], add) / fact(b[ax]);
-              }
-              if (!ok) continue;
-              const double val = KIND == VEL ? S[Idx<D>::template flat<n>(q)]
-                                             : W[Idx<D>::template flat<n>(q)];
-              kpart = fma(coef, val, kpart);
-            }
-          }
-          acc = fma(P.G[k], kpart, acc);
+        for (int e = 0; e < E; ++e) {
+          const int qc = (e / stride) % n;
+          const double dv = qc + 1 < n ? __ddiv_rn(__dmul_rn(Pt[e + stride], static_cast<double>(qc + 1)), P.h) : 0.0;
+          Vt[c * E + e] = __dmul_rn(P.av, dv);
         }
-        double* ptr = dst + toff + f * P.t_coef;
-        const double nv = *ptr + acc;
-        bad |= !isfinite(nv);
-        *ptr = nv;
       }
-    }
-  } else {
-    // 3'. iterated truncated recurrence with per-node ap jets and scalar av
-    const double* apj = P.coeff + static_cast<int64_t>(D == 3 ? t[2] : 0) * P.c_layer +
-                        static_cast<int64_t>(D >= 2 ? t[1] : 0) * P.tNx + t[0];
-    double acc_out[KIND == VEL ? D * F : F];
+    } else {
+      // Pt <- ap (.) (sum_c d_c V_c); the sum goes through S as scratch
 #pragma unroll 1
-    for (int i = 0; i < (KIND == VEL ? D * F : F); ++i) acc_out[i] = 0.0;
-    double tmp[E];
+      for (int e = 0; e < E; ++e) S[e] = 0.0;
 #pragma unroll 1
-    for (int r = 0; r + 1 < n; ++r) {
-      // which table is non-zero at level r: VEL seeds P (even r -> P), PRE seeds V
-      const bool p_live = (KIND == VEL) == (r % 2 == 0);
-      if (p_live) {
-        // V_c[r+1] = av d_c P[r]
+      for (int c = 0; c < D; ++c) {
+        const int stride = cpow(n, D - 1 - c);
 #pragma unroll 1
-        for (int c = 0; c < D; ++c) {
-          const int stride = cpow(n, D - 1 - c);
-#pragma unroll 1
-          for (int e = 0; e < E; ++e) {
-            const int qc = (e / stride) % n;
-            Vt[c * E + e] = qc + 1 < n ? P.av * (Pt[e + stride] * (qc + 1) * P.inv_h) : 0.0;
-          }
+        for (int e = 0; e < E; ++e) {
+          const int qc = (e / stride) % n;
+          const double dv = qc + 1 < n ? __ddiv_rn(__dmul_rn(Vt[c * E + e + stride], static_cast<double>(qc + 1)), P.h) : 0.0;
+          S[e] = __dadd_rn(S[e], dv);
         }
-        if (KIND == VEL && ((r + 1) & 1)) {
-#pragma unroll 1
-          for (int c = 0; c < D; ++c)
-#pragma unroll 1
-            for (int f = 0; f < F; ++f) {
-              int o[3] = {0, 0, 0};
-              Idx<D>::template split<n1>(f, o);
-              acc_out[c * F + f] = fma(P.w[r + 1], Vt[c * E + Idx<D>::template flat<n>(o)], acc_out[c * F + f]);
-            }
-        }
-      } else {
-        // P[r+1] = ap (.) sum_c d_c V_c[r]
-#pragma unroll 1
-        for (int e = 0; e < E; ++e) tmp[e] = 0.0;
-#pragma unroll 1
-        for (int c = 0; c < D; ++c) {
-          const int stride = cpow(n, D - 1 - c);
-#pragma unroll 1
-          for (int e = 0; e < E; ++e) {
-            const int qc = (e / stride) % n;
-            if (qc + 1 < n) tmp[e] += Vt[c * E + e + stride] * (qc + 1) * P.inv_h;
-          }
-        }
-        // truncated tensor product (jet.cpp:109-121)
+      }
+      if (VAR) {
+        // truncated tensor product, contributions in ascending order of the
+        // ap index (jet.cpp:109-121)
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
           int q[3] = {0, 0, 0};
@@ -294,31 +215,41 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
               if (qr[ax] < 0) ok = false;
             }
             if (!ok) continue;
-            s = fma(__ldg(apj + ei * P.c_coef), tmp[Idx<D>::template flat<n>(qr)], s);
+            const double a = __ldg(apj + ei * P.c_coef);
+            if (a == 0.0) continue;
+            s = __dadd_rn(s, __dmul_rn(a, S[Idx<D>::template flat<n>(qr)]));
           }
           Pt[e] = s;
         }
-        if (KIND == PRE && ((r + 1) & 1)) {
+      } else {
 #pragma unroll 1
-          for (int f = 0; f < F; ++f) {
-            int o[3] = {0, 0, 0};
-            Idx<D>::template split<n1>(f, o);
-            acc_out[f] = fma(P.w[r + 1], Pt[Idx<D>::template flat<n>(o)], acc_out[f]);
-          }
-        }
+        for (int e = 0; e < E; ++e) Pt[e] = __dmul_rn(P.ap, S[e]);
       }
     }
-    constexpr int NOUT = KIND == VEL ? D : 1;
+    // leapfrog_half_update (stepper1d.cpp:54-61): odd levels of the target's table
+    if ((r + 1) & 1) {
+      const double w = P.w[r + 1];
 #pragma unroll 1
-    for (int c = 0; c < NOUT; ++c)
+      for (int c = 0; c < NOUT; ++c)
 #pragma unroll 1
-      for (int f = 0; f < F; ++f) {
-        double* ptr = P.dst[c] + toff + f * P.t_coef;
-        const double nv = *ptr + acc_out[c * F + f];
-        bad |= !isfinite(nv);
-        *ptr = nv;
-      }
+        for (int f = 0; f < F; ++f) {
+          int o[3] = {0, 0, 0};
+          Idx<D>::template split<n1>(f, o);
+          const int e = Idx<D>::template flat<n>(o);
+          const double tv = KIND == VEL ? Vt[c * E + e] : Pt[e];
+          tgt[c * F + f] = __dadd_rn(tgt[c * F + f], __dmul_rn(w, tv));
+        }
+    }
   }
+  // 4. in-place store + finite flag (check_finite, stepper1d.cpp:121-129)
+#pragma unroll 1
+  for (int c = 0; c < NOUT; ++c)
+#pragma unroll 1
+    for (int f = 0; f < F; ++f) {
+      const double nv = tgt[c * F + f];
+      bad |= !isfinite(nv);
+      P.dst[c][toff + f * P.t_coef] = nv;
+    }
 
   if (bad && P.step >= 0) atomicMin(P.flag, P.step);
 }

@@ -1,7 +1,371 @@
-// Tiled 3D half-step kernels (placeholder until the z-marching kernel lands).
+// Tiled, z-marching 3D half-step kernel (d = 3, constant coefficients, m <= 3).
+//
+// One CTA = 8 warps owns a row of TXC = 32 target cells along x (lane = cell)
+// and marches over a chunk of ZC target layers in z.  Per target layer k it
+//   (raw)  streams the next source layer (all (m+1)^3 coefficients of the
+//          33 x 2 source nodes under the row) into shared memory with cp.async,
+//          one layer ahead of use;
+//   (X)    applies M along x: 2 (m+1)^2 x-lines per cell, shared by the two
+//          source rows (reconstruct_cell_2d's first sweep, interpolation.cpp:87-99);
+//   (Y)    applies M along y: n (m+1) y-lines per cell (interpolation.cpp:101-112);
+//          the result for source layer k+1 goes into a 2-layer ring;
+//   (Z+CK) applies M along z between ring layers k and k+1 and immediately
+//          contracts with the closed-form odd Cauchy-Kowalewski sum of the
+//          leapfrog half update (stepper1d.cpp:22-61).
+// Every line uses the parity split of M (out[s] couples to sigma_l = L_l + R_l
+// for s+l even and to delta_l = R_l - L_l for s+l odd),
+// with rows pre-scaled by s! so that the CK coefficients collapse to
+// G_k k!/b! (host table GM) and a final 1/o! per output.
+// Warps specialise by parity class in the Z+CK stage: warp w owns the P
+// entries with (q_x, q_y, q_z) = (w>>2, w>>1, w) mod 2, which holds every P
+// entry any of its 24 (velocity) or 8 (pressure) outputs needs, so the CK sum
+// runs entirely in registers with compile-time indices.
+//
+// VEL (p -> v_x, v_y, v_z) is one launch; PRE (v -> p) is three launches, one
+// per source component c, each adding the c-th divergence term (q_c+1)V_c[q+e_c]
+// through the same code with target component c.
+#include <cstring>
+#include <type_traits>
+#include <utility>
+
 #include "hlf_internal.cuh"
 
 namespace hlfk {
-bool tiled3d_supported(int) { return false; }
-int launch_half_tiled3d(int, HalfKind, const HalfParams&, cudaStream_t) { return -1; }
+namespace {
+
+constexpr int TXC = 32;         // cells per CTA row (= lanes)
+constexpr int RAWX = TXC + 1;   // source nodes per row
+constexpr int NWARP = 8;
+constexpr int NTHREADS = NWARP * 32;
+constexpr int ZC = 32;          // target layers per CTA
+constexpr int kMaxB = 20;       // multi-indices |b| <= 3
+
+template <int MM>
+struct Cfg {
+  static constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1 * n1;
+  static constexpr int RAW = F * 2 * RAWX;
+  static constexpr int XB = n1 * n1 * n * 2 * TXC;
+  static constexpr int RING = n * n * n1 * TXC;
+  static constexpr int SMEM_DOUBLES = RAW + XB + 2 * RING;
+  static constexpr int RAW_PER_THREAD = (RAW + NTHREADS - 1) / NTHREADS;
+};
+
+struct TParams {
+  double ML[kMaxN * (kMaxM + 1)];  // s! * M[s][l], l < m+1 (left block), row-major [s][l]
+  double GM[kMaxB];                // G_k * k!/b!, indexed by bindex(b)
+  const double* src;               // source field base (layer 0 of the allocation)
+  double* dst[3];                  // target field bases, per target component
+  int64_t s_layer, s_plane;        // source strides
+  int64_t t_layer, t_plane;        // target strides
+  int sNx, sNy;                    // source plane dims (row stride = sNx)
+  int tNx, tNy, tNz;               // target nodes
+  int t_zoff;                      // target layer index of z = 0
+  int K[2], bnd[2];                // x, y cells and boundary kinds
+  int pre;                         // 1: source is the dual family (x0 - 1 shift, mirrors)
+  int comp;                        // source component (mirror parity), PRE only
+  int step;
+  int* flag;
+};
+
+__host__ __device__ constexpr int bindex(int b0, int b1, int b2, int mm) {
+  // position of (b0, b1, b2) in the enumeration b0 <= mm, b1 <= mm-b0, b2 <= mm-b0-b1
+  int idx = 0;
+  for (int a0 = 0; a0 <= mm; ++a0)
+    for (int a1 = 0; a1 <= mm - a0; ++a1)
+      for (int a2 = 0; a2 <= mm - a0 - a1; ++a2) {
+        if (a0 == b0 && a1 == b1 && a2 == b2) return idx;
+        ++idx;
+      }
+  return -1;
+}
+
+__host__ __device__ constexpr double ifact(int k) {
+  double r = 1.0;
+  for (int t = 2; t <= k; ++t) r *= t;
+  return 1.0 / r;
+}
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// full parity-split line: L, R = the two endpoint jets (m+1 each) -> n outputs
+template <int MM>
+__device__ __forceinline__ void line_full(const TParams& P, const double (&L)[MM + 1],
+                                          const double (&R)[MM + 1], double (&out)[2 * MM + 2]) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  double sg[n1], dl[n1];
+#pragma unroll
+  for (int l = 0; l < n1; ++l) {
+    sg[l] = L[l] + R[l];
+    dl[l] = R[l] - L[l];
+  }
+#pragma unroll
+  for (int s = 0; s < n; ++s) {
+    double acc = 0.0;
+#pragma unroll
+    for (int l = 0; l < n1; ++l) {
+      if (((s + l) & 1) == 0) acc = fma(P.ML[s * n1 + l], sg[l], acc);
+      else acc = fma(-P.ML[s * n1 + l], dl[l], acc);
+    }
+    out[s] = acc;
+  }
+}
+
+#include "tiled3d_gen.cuh"
+
+// raw source layer -> shared memory, cp.async 8 B per element (one layer ahead)
+template <int MM>
+__device__ __forceinline__ void issue_raw(double* raw, const double* base, const int* off, int tid) {
+  using G = Cfg<MM>;
+#pragma unroll
+  for (int t = 0; t < G::RAW_PER_THREAD; ++t)
+    if (off[t] >= 0) cp_async8(raw + tid + t * NTHREADS, base + off[t]);
+  cp_async_commit();
+}
+
+template <int MM>
+__device__ __forceinline__ void finish_raw(double* raw, unsigned negmask, int tid) {
+  using G = Cfg<MM>;
+  cp_async_wait_all();
+  if (negmask) {
+#pragma unroll
+    for (int t = 0; t < G::RAW_PER_THREAD; ++t)
+      if ((negmask >> t) & 1u) raw[tid + t * NTHREADS] = -raw[tid + t * NTHREADS];
+  }
+  __syncthreads();
+}
+
+// X stage: x-lines between source nodes i, i+1 for every (l_y, l_z) and source row
+template <int MM>
+__device__ __forceinline__ void x_stage(const TParams& P, const double* raw, double* xb, int warp, int lane) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+#pragma unroll 1
+  for (int t = warp; t < 2 * n1 * n1; t += NWARP) {
+    const int sy = t / (n1 * n1), lylz = t - sy * n1 * n1;
+    double L[n1], R[n1], out[n];
+#pragma unroll
+    for (int lx = 0; lx < n1; ++lx) {
+      const double* rp = raw + ((lx * n1 * n1 + lylz) * 2 + sy) * RAWX + lane;
+      L[lx] = rp[0];
+      R[lx] = rp[1];
+    }
+    line_full<MM>(P, L, R, out);
+#pragma unroll
+    for (int s = 0; s < n; ++s) xb[((lylz * n + s) * 2 + sy) * TXC + lane] = out[s];
+  }
+}
+
+// Y stage: y-lines between the two source rows for every (q_x, l_z)
+template <int MM>
+__device__ __forceinline__ void y_stage(const TParams& P, const double* xb, double* rg, int warp, int lane) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+#pragma unroll 1
+  for (int t = warp; t < n * n1; t += NWARP) {
+    const int qx = t / n1, lz = t - qx * n1;
+    double L[n1], R[n1], out[n];
+#pragma unroll
+    for (int ly = 0; ly < n1; ++ly) {
+      const double* xp = xb + (((ly * n1 + lz) * n + qx) * 2) * TXC + lane;
+      L[ly] = xp[0];
+      R[ly] = xp[TXC];
+    }
+    line_full<MM>(P, L, R, out);
+#pragma unroll
+    for (int s = 0; s < n; ++s) rg[((qx * n + s) * n1 + lz) * TXC + lane] = out[s];
+  }
+}
+
+template <int MM, int NT, int CSOLE>
+__device__ __forceinline__ void zck(int w, const TParams& P, const double* ro, const double* rn, int lane,
+                                    double* const* dptr, bool active, bool& bad) {
+  if constexpr (MM == 1) {
+    if constexpr (NT == 3) zck_m1_vel(w, P, ro, rn, lane, dptr, active, bad);
+    else if constexpr (CSOLE == 0) zck_m1_pre0(w, P, ro, rn, lane, dptr, active, bad);
+    else if constexpr (CSOLE == 1) zck_m1_pre1(w, P, ro, rn, lane, dptr, active, bad);
+    else zck_m1_pre2(w, P, ro, rn, lane, dptr, active, bad);
+  } else if constexpr (MM == 2) {
+    if constexpr (NT == 3) zck_m2_vel(w, P, ro, rn, lane, dptr, active, bad);
+    else if constexpr (CSOLE == 0) zck_m2_pre0(w, P, ro, rn, lane, dptr, active, bad);
+    else if constexpr (CSOLE == 1) zck_m2_pre1(w, P, ro, rn, lane, dptr, active, bad);
+    else zck_m2_pre2(w, P, ro, rn, lane, dptr, active, bad);
+  } else {
+    if constexpr (NT == 3) zck_m3_vel(w, P, ro, rn, lane, dptr, active, bad);
+    else if constexpr (CSOLE == 0) zck_m3_pre0(w, P, ro, rn, lane, dptr, active, bad);
+    else if constexpr (CSOLE == 1) zck_m3_pre1(w, P, ro, rn, lane, dptr, active, bad);
+    else zck_m3_pre2(w, P, ro, rn, lane, dptr, active, bad);
+  }
+}
+
+template <int MM, int NT, int CSOLE>
+__global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ TParams P) {
+  using G = Cfg<MM>;
+  constexpr int n1 = G::n1;
+  extern __shared__ __align__(16) double smem[];
+  double* raw = smem;
+  double* xb = raw + G::RAW;
+  double* ring0 = xb + G::XB;
+  double* ring1 = ring0 + G::RING;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int x0 = blockIdx.x * TXC;
+  const int ty = blockIdx.y;
+  const int k0 = blockIdx.z * ZC;
+  const int k1 = min(k0 + ZC, P.tNz);
+  if (k0 >= k1) return;
+  const bool active = x0 + lane < P.tNx;
+
+  // per-thread raw-element offsets (the same for every layer) and mirror signs
+  int off[G::RAW_PER_THREAD];
+  unsigned negmask = 0;
+#pragma unroll 1
+  for (int t = 0; t < G::RAW_PER_THREAD; ++t) {
+    const int e = tid + t * NTHREADS;
+    off[t] = -1;
+    if (e >= G::RAW) continue;
+    const int f = e / (2 * RAWX);
+    const int r = e - f * 2 * RAWX;
+    const int sy = r / RAWX, sx = r - sy * RAWX;
+    int q0 = x0 + sx - P.pre, q1 = ty + sy - P.pre;
+    bool neg = false;
+    const int ax0 = f / (n1 * n1), ay0 = (f / n1) % n1;
+    // x
+    if (P.bnd[0] == 0) {
+      if (q0 >= P.K[0]) q0 -= P.K[0];
+      if (q0 < 0) q0 += P.K[0];
+    } else if (P.pre && (q0 < 0 || q0 == P.K[0])) {
+      q0 = q0 < 0 ? 0 : P.K[0] - 1;
+      neg ^= (ax0 & 1) != 0;
+      neg ^= P.comp != 0;
+    }
+    if (q0 >= P.sNx) q0 = P.sNx - 1;
+    // y
+    if (P.bnd[1] == 0) {
+      if (q1 >= P.K[1]) q1 -= P.K[1];
+      if (q1 < 0) q1 += P.K[1];
+    } else if (P.pre && (q1 < 0 || q1 == P.K[1])) {
+      q1 = q1 < 0 ? 0 : P.K[1] - 1;
+      neg ^= (ay0 & 1) != 0;
+      neg ^= P.comp != 1;
+    }
+    if (q1 >= P.sNy) q1 = P.sNy - 1;
+    off[t] = static_cast<int>(f * P.s_plane + static_cast<int64_t>(q1) * P.sNx + q0);
+    if (neg) negmask |= 1u << t;
+  }
+
+  // prologue: source layer k0 -> ring0; raw for k0 + 1 in flight
+  issue_raw<MM>(raw, P.src + static_cast<int64_t>(k0) * P.s_layer, off, tid);
+  finish_raw<MM>(raw, negmask, tid);
+  x_stage<MM>(P, raw, xb, warp, lane);
+  __syncthreads();
+  issue_raw<MM>(raw, P.src + static_cast<int64_t>(k0 + 1) * P.s_layer, off, tid);
+  y_stage<MM>(P, xb, ring0, warp, lane);
+  double* ro = ring0;
+  double* rn = ring1;
+  bool bad = false;
+#pragma unroll 1
+  for (int k = k0; k < k1; ++k) {
+    finish_raw<MM>(raw, negmask, tid);  // raw(k+1) landed; orders the previous Z stage before this Y stage
+    x_stage<MM>(P, raw, xb, warp, lane);
+    __syncthreads();
+    if (k + 1 < k1) issue_raw<MM>(raw, P.src + static_cast<int64_t>(k + 2) * P.s_layer, off, tid);
+    y_stage<MM>(P, xb, rn, warp, lane);
+    __syncthreads();
+    double* dptr[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+      dptr[t] = P.dst[t] + static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + lane;
+    zck<MM, NT, CSOLE>(warp, P, ro, rn, lane, dptr, active, bad);
+    double* tmp = ro;
+    ro = rn;
+    rn = tmp;
+  }
+  if (bad && active && P.step >= 0) atomicMin(P.flag, P.step);
+}
+
+double host_fact(int k) {
+  double r = 1.0;
+  for (int t = 2; t <= k; ++t) r *= t;
+  return r;
+}
+
+template <int MM, int NT, int CSOLE>
+int launch_one(const TParams& T, cudaStream_t st) {
+  using G = Cfg<MM>;
+  const size_t smem = sizeof(double) * G::SMEM_DOUBLES;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tiled3d<MM, NT, CSOLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+  dim3 grid((T.tNx + TXC - 1) / TXC, T.tNy, (T.tNz + ZC - 1) / ZC);
+  tiled3d<MM, NT, CSOLE><<<grid, NTHREADS, smem, st>>>(T);
+  return 1;
+}
+
+template <int MM>
+int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  TParams T;
+  std::memset(&T, 0, sizeof(T));
+  for (int s = 0; s < n; ++s)
+    for (int l = 0; l < n1; ++l) T.ML[s * n1 + l] = host_fact(s) * p.M[s * n + l];
+  for (int b0 = 0; b0 <= MM; ++b0)
+    for (int b1 = 0; b1 <= MM - b0; ++b1)
+      for (int b2 = 0; b2 <= MM - b0 - b1; ++b2) {
+        const int k = b0 + b1 + b2;
+        T.GM[bindex(b0, b1, b2, MM)] = p.G[k] * host_fact(k) / (host_fact(b0) * host_fact(b1) * host_fact(b2));
+      }
+  T.s_layer = p.s_layer;
+  T.s_plane = p.s_coef;
+  T.t_layer = p.t_layer;
+  T.t_plane = p.t_coef;
+  T.sNx = p.sNx;
+  T.sNy = p.sNy;
+  T.tNx = p.tNx;
+  T.tNy = p.tNy;
+  T.tNz = p.tNz;
+  T.t_zoff = p.t_zoff;
+  T.K[0] = p.K[0];
+  T.K[1] = p.K[1];
+  T.bnd[0] = p.bnd[0];
+  T.bnd[1] = p.bnd[1];
+  T.step = p.step;
+  T.flag = p.flag;
+  if (kind == VEL) {
+    T.pre = 0;
+    T.comp = 0;
+    T.src = p.src[0];
+    for (int t = 0; t < 3; ++t) T.dst[t] = p.dst[t];
+    return launch_one<MM, 3, 0>(T, st);
+  }
+  T.pre = 1;
+  int launched = 0;
+  for (int c = 0; c < 3; ++c) {
+    T.comp = c;
+    T.src = p.src[c];
+    T.dst[0] = p.dst[0];
+    if (c == 0) launched += launch_one<MM, 1, 0>(T, st);
+    else if (c == 1) launched += launch_one<MM, 1, 1>(T, st);
+    else launched += launch_one<MM, 1, 2>(T, st);
+  }
+  return launched;
+}
+
+}  // namespace
+
+bool tiled3d_supported(int m) { return m >= 1 && m <= 3; }
+
+int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st) {
+  switch (m) {
+    case 1: return launch_m<1>(kind, p, st);
+    case 2: return launch_m<2>(kind, p, st);
+    case 3: return launch_m<3>(kind, p, st);
+    default: return -1;
+  }
+}
+
 }  // namespace hlfk

@@ -105,10 +105,26 @@ def test_parity_3d_generic(m, boundary):
 
 
 @pytest.mark.parametrize("m", [1, 2, 3])
-def test_parity_3d_default_kernel(m):
-    g, o = make_pair(3, m, [16, 12, 10], seed=40 + m)
+@pytest.mark.parametrize("boundary", [[0, 0, 0], [1, 1, 1], [1, 0, 0], [0, 1, 1]])
+def test_parity_3d_tiled_kernel(m, boundary):
+    # K crosses a partial 32-cell x tile and two 32-layer z chunks
+    g, o = make_pair(3, m, [36, 4, 40], boundary=boundary, seed=40 + m)
+    assert g.kernel_variant == 1
     run_both(g, o, 3, 0.25 * g.grid.h)
     compare(g, o, 3)
+
+
+def test_tiled_equals_generic_long_run():
+    # the tiled kernel reorders the arithmetic (parity split, FMA); over a long
+    # run the two GPU kernels differ by the reconstruction's roundoff floor only
+    ga, _ = make_pair(3, 3, [32, 8, 8], seed=77)
+    gb, _ = make_pair(3, 3, [32, 8, 8], seed=77)
+    gb.kernel_variant = 0
+    for s in (ga, gb):
+        s.set_times(0, 0.02, 0.04)
+        s.advance_n(50)
+    for f in range(4):
+        assert rel_err(ga.get_field(f), gb.get_field(f)) <= 1e-10
 
 
 def c2_jets(d, K, h, n, boundary, dual):
