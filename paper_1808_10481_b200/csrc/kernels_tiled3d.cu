@@ -42,17 +42,20 @@ constexpr int kMaxB = 20;       // multi-indices |b| <= 3
 
 template <int MM>
 struct Cfg {
-  static constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1 * n1;
+  static constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1 * n1, nh = n / 2, jh = (n1 + 1) / 2;
   static constexpr int RAW = F * 2 * RAWX;
-  static constexpr int XB = n1 * n1 * n * 2 * TXC;
   static constexpr int RING = n * n * n1 * TXC;
-  static constexpr int SMEM_DOUBLES = RAW + XB + 2 * RING;
   static constexpr int RAW_PER_THREAD = (RAW + NTHREADS - 1) / NTHREADS;
+  template <int NT>
+  static constexpr int TGT = NT * F * TXC;
+  template <int NT>
+  static constexpr int SMEM_DOUBLES = RAW + 2 * RING + TGT<NT>;
 };
 
 struct TParams {
   double ML[kMaxN * (kMaxM + 1)];  // s! * M[s][l], l < m+1 (left block), row-major [s][l]
   double GM[kMaxB];                // G_k * k!/b!, indexed by bindex(b)
+  double IF[kMaxM + 1];            // 1/o!
   const double* src;               // source field base (layer 0 of the allocation)
   double* dst[3];                  // target field bases, per target component
   int64_t s_layer, s_plane;        // source strides
@@ -92,32 +95,8 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-// full parity-split line: L, R = the two endpoint jets (m+1 each) -> n outputs
-template <int MM>
-__device__ __forceinline__ void line_full(const TParams& P, const double (&L)[MM + 1],
-                                          const double (&R)[MM + 1], double (&out)[2 * MM + 2]) {
-  constexpr int n1 = MM + 1, n = 2 * MM + 2;
-  double sg[n1], dl[n1];
-#pragma unroll
-  for (int l = 0; l < n1; ++l) {
-    sg[l] = L[l] + R[l];
-    dl[l] = R[l] - L[l];
-  }
-#pragma unroll
-  for (int s = 0; s < n; ++s) {
-    double acc = 0.0;
-#pragma unroll
-    for (int l = 0; l < n1; ++l) {
-      if (((s + l) & 1) == 0) acc = fma(P.ML[s * n1 + l], sg[l], acc);
-      else acc = fma(-P.ML[s * n1 + l], dl[l], acc);
-    }
-    out[s] = acc;
-  }
-}
-
 #include "tiled3d_gen.cuh"
 
-// raw source layer -> shared memory, cp.async 8 B per element (one layer ahead)
 template <int MM>
 __device__ __forceinline__ void issue_raw(double* raw, const double* base, const int* off, int tid) {
   using G = Cfg<MM>;
@@ -128,87 +107,52 @@ __device__ __forceinline__ void issue_raw(double* raw, const double* base, const
 }
 
 template <int MM>
-__device__ __forceinline__ void finish_raw(double* raw, unsigned negmask, int tid) {
-  using G = Cfg<MM>;
-  cp_async_wait_all();
-  if (negmask) {
-#pragma unroll
-    for (int t = 0; t < G::RAW_PER_THREAD; ++t)
-      if ((negmask >> t) & 1u) raw[tid + t * NTHREADS] = -raw[tid + t * NTHREADS];
-  }
-  __syncthreads();
-}
-
-// X stage: x-lines between source nodes i, i+1 for every (l_y, l_z) and source row
-template <int MM>
-__device__ __forceinline__ void x_stage(const TParams& P, const double* raw, double* xb, int warp, int lane) {
-  constexpr int n1 = MM + 1, n = 2 * MM + 2;
-#pragma unroll 1
-  for (int t = warp; t < 2 * n1 * n1; t += NWARP) {
-    const int sy = t / (n1 * n1), lylz = t - sy * n1 * n1;
-    double L[n1], R[n1], out[n];
-#pragma unroll
-    for (int lx = 0; lx < n1; ++lx) {
-      const double* rp = raw + ((lx * n1 * n1 + lylz) * 2 + sy) * RAWX + lane;
-      L[lx] = rp[0];
-      R[lx] = rp[1];
-    }
-    line_full<MM>(P, L, R, out);
-#pragma unroll
-    for (int s = 0; s < n; ++s) xb[((lylz * n + s) * 2 + sy) * TXC + lane] = out[s];
-  }
-}
-
-// Y stage: y-lines between the two source rows for every (q_x, l_z)
-template <int MM>
-__device__ __forceinline__ void y_stage(const TParams& P, const double* xb, double* rg, int warp, int lane) {
-  constexpr int n1 = MM + 1, n = 2 * MM + 2;
-#pragma unroll 1
-  for (int t = warp; t < n * n1; t += NWARP) {
-    const int qx = t / n1, lz = t - qx * n1;
-    double L[n1], R[n1], out[n];
-#pragma unroll
-    for (int ly = 0; ly < n1; ++ly) {
-      const double* xp = xb + (((ly * n1 + lz) * n + qx) * 2) * TXC + lane;
-      L[ly] = xp[0];
-      R[ly] = xp[TXC];
-    }
-    line_full<MM>(P, L, R, out);
-#pragma unroll
-    for (int s = 0; s < n; ++s) rg[((qx * n + s) * n1 + lz) * TXC + lane] = out[s];
-  }
-}
-
-template <int MM, int NT, int CSOLE>
-__device__ __forceinline__ void zck(int w, const TParams& P, const double* ro, const double* rn, int lane,
-                                    double* const* dptr, bool active, bool& bad) {
+__device__ __forceinline__ void xy_task(const TParams& P, int w, const double* raw, double* rn, int lane) {
+  // task w = (l_z, q_x parity): fused X+Y stage into the ring layer rn
+  constexpr int n1 = MM + 1;
+  if (w >= 2 * n1) return;
+  const int lz = w >> 1;
+  const double* rb = raw + lz * 2 * RAWX + lane;
+  double* wb = rn + lz * TXC + lane;
   if constexpr (MM == 1) {
-    if constexpr (NT == 3) zck_m1_vel(w, P, ro, rn, lane, dptr, active, bad);
-    else if constexpr (CSOLE == 0) zck_m1_pre0(w, P, ro, rn, lane, dptr, active, bad);
-    else if constexpr (CSOLE == 1) zck_m1_pre1(w, P, ro, rn, lane, dptr, active, bad);
-    else zck_m1_pre2(w, P, ro, rn, lane, dptr, active, bad);
+    if (w & 1) m1_xy_px1(P, rb, wb); else m1_xy_px0(P, rb, wb);
   } else if constexpr (MM == 2) {
-    if constexpr (NT == 3) zck_m2_vel(w, P, ro, rn, lane, dptr, active, bad);
-    else if constexpr (CSOLE == 0) zck_m2_pre0(w, P, ro, rn, lane, dptr, active, bad);
-    else if constexpr (CSOLE == 1) zck_m2_pre1(w, P, ro, rn, lane, dptr, active, bad);
-    else zck_m2_pre2(w, P, ro, rn, lane, dptr, active, bad);
+    if (w & 1) m2_xy_px1(P, rb, wb); else m2_xy_px0(P, rb, wb);
   } else {
-    if constexpr (NT == 3) zck_m3_vel(w, P, ro, rn, lane, dptr, active, bad);
-    else if constexpr (CSOLE == 0) zck_m3_pre0(w, P, ro, rn, lane, dptr, active, bad);
-    else if constexpr (CSOLE == 1) zck_m3_pre1(w, P, ro, rn, lane, dptr, active, bad);
-    else zck_m3_pre2(w, P, ro, rn, lane, dptr, active, bad);
+    if (w & 1) m3_xy_px1(P, rb, wb); else m3_xy_px0(P, rb, wb);
   }
 }
 
-template <int MM, int NT, int CSOLE>
+template <int MM>
+__device__ __forceinline__ void z_stage(const TParams& P, int pz, const double* ro, const double* rn,
+                                        double (&pt)[MM + 1][MM + 1][MM + 1]) {
+  if constexpr (MM == 1) {
+    if (pz) m1_z_pz1(P, ro, rn, pt); else m1_z_pz0(P, ro, rn, pt);
+  } else if constexpr (MM == 2) {
+    if (pz) m2_z_pz1(P, ro, rn, pt); else m2_z_pz0(P, ro, rn, pt);
+  } else {
+    if (pz) m3_z_pz1(P, ro, rn, pt); else m3_z_pz0(P, ro, rn, pt);
+  }
+}
+
+template <int MM>
+__device__ __forceinline__ void ck(int c, int w, const TParams& P, const double (&pt)[MM + 1][MM + 1][MM + 1],
+                                   double (&acc)[(MM + 2) / 2][(MM + 2) / 2][(MM + 2) / 2]) {
+  if constexpr (MM == 1) m1_ck(c, w, P, pt, acc);
+  else if constexpr (MM == 2) m2_ck(c, w, P, pt, acc);
+  else m3_ck(c, w, P, pt, acc);
+}
+
+template <int MM, int NT>
 __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ TParams P) {
   using G = Cfg<MM>;
-  constexpr int n1 = G::n1;
+  constexpr int n1 = G::n1, n = G::n, F = G::F, nh = G::nh, jh = G::jh;
+  static_assert(nh == MM + 1, "n/2 == m+1");
   extern __shared__ __align__(16) double smem[];
   double* raw = smem;
-  double* xb = raw + G::RAW;
-  double* ring0 = xb + G::XB;
+  double* ring0 = raw + G::RAW;
   double* ring1 = ring0 + G::RING;
+  double* tgs = ring1 + G::RING;  // targets of the current layer [t][f][cell]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int x0 = blockIdx.x * TXC;
@@ -232,7 +176,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
     int q0 = x0 + sx - P.pre, q1 = ty + sy - P.pre;
     bool neg = false;
     const int ax0 = f / (n1 * n1), ay0 = (f / n1) % n1;
-    // x
     if (P.bnd[0] == 0) {
       if (q0 >= P.K[0]) q0 -= P.K[0];
       if (q0 < 0) q0 += P.K[0];
@@ -242,7 +185,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
       neg ^= P.comp != 0;
     }
     if (q0 >= P.sNx) q0 = P.sNx - 1;
-    // y
     if (P.bnd[1] == 0) {
       if (q1 >= P.K[1]) q1 -= P.K[1];
       if (q1 < 0) q1 += P.K[1];
@@ -255,30 +197,83 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
     off[t] = static_cast<int>(f * P.s_plane + static_cast<int64_t>(q1) * P.sNx + q0);
     if (neg) negmask |= 1u << t;
   }
+  auto finish_raw = [&]() {  // (tiny; kept inline)
+    cp_async_wait_all();
+    if (negmask) {
+#pragma unroll 1
+      for (int t = 0; t < G::RAW_PER_THREAD; ++t)
+        if ((negmask >> t) & 1u) raw[tid + t * NTHREADS] = -raw[tid + t * NTHREADS];
+    }
+    __syncthreads();
+  };
 
-  // prologue: source layer k0 -> ring0; raw for k0 + 1 in flight
+  // class of this warp in the Z + CK stage
+  const int PX = (warp >> 2) & 1, PY = (warp >> 1) & 1, PZ = warp & 1;
+  const int cbase = ((PX * n + PY) * n1) * TXC + lane;
+
+  // iteration k0-1 is the prologue: it only builds ring layer k0
   issue_raw<MM>(raw, P.src + static_cast<int64_t>(k0) * P.s_layer, off, tid);
-  finish_raw<MM>(raw, negmask, tid);
-  x_stage<MM>(P, raw, xb, warp, lane);
-  __syncthreads();
-  issue_raw<MM>(raw, P.src + static_cast<int64_t>(k0 + 1) * P.s_layer, off, tid);
-  y_stage<MM>(P, xb, ring0, warp, lane);
-  double* ro = ring0;
-  double* rn = ring1;
+  double* ro = ring1;
+  double* rn = ring0;
   bool bad = false;
 #pragma unroll 1
-  for (int k = k0; k < k1; ++k) {
-    finish_raw<MM>(raw, negmask, tid);  // raw(k+1) landed; orders the previous Z stage before this Y stage
-    x_stage<MM>(P, raw, xb, warp, lane);
+  for (int k = k0 - 1; k < k1; ++k) {
+    const bool work = k >= k0;
+    finish_raw();  // raw(k+1) landed; every warp left the previous Z + CK stage
+    if (work) {
+      // targets of layer k -> smem (async; consumed after the XY stage)
+      const int64_t lbase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0;
+#pragma unroll 1
+      for (int e = tid; e < NT * F * TXC; e += NTHREADS) {
+        const int cell = e & (TXC - 1);
+        const int tf = e >> 5;
+        const int t = tf / F, f = tf - t * F;
+        if (x0 + cell < P.tNx) cp_async8(tgs + e, P.dst[t] + lbase + f * P.t_plane + cell);
+      }
+      cp_async_commit();
+    }
+    xy_task<MM>(P, warp, raw, rn, lane);
+    cp_async_wait_all();
     __syncthreads();
     if (k + 1 < k1) issue_raw<MM>(raw, P.src + static_cast<int64_t>(k + 2) * P.s_layer, off, tid);
-    y_stage<MM>(P, xb, rn, warp, lane);
-    __syncthreads();
-    double* dptr[NT];
+
+    if (work) {
+      // Z stage + CK for this warp's parity class
+      double pt[nh][nh][nh];
+      z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
+      const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + lane;
+#pragma unroll 1
+      for (int t = 0; t < NT; ++t) {
+        const int c = NT == 3 ? t : P.comp;
+        double acc[jh][jh][jh];
 #pragma unroll
-    for (int t = 0; t < NT; ++t)
-      dptr[t] = P.dst[t] + static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + lane;
-    zck<MM, NT, CSOLE>(warp, P, ro, rn, lane, dptr, active, bad);
+        for (int a = 0; a < jh; ++a)
+#pragma unroll
+          for (int b = 0; b < jh; ++b)
+#pragma unroll
+            for (int d = 0; d < jh; ++d) acc[a][b][d] = 0.0;
+        ck<MM>(c, warp, P, pt, acc);
+        double* dstt = P.dst[t];
+        const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
+#pragma unroll
+        for (int a = 0; a < jh; ++a) {
+          const int ox = sx + 2 * a;
+#pragma unroll
+          for (int b = 0; b < jh; ++b) {
+            const int oy = sy + 2 * b;
+#pragma unroll
+            for (int d = 0; d < jh; ++d) {
+              const int oz = sz + 2 * d;
+              if (ox > MM || oy > MM || oz > MM) continue;
+              const int f = (ox * n1 + oy) * n1 + oz;
+              const double v = fma(acc[a][b][d], P.IF[ox] * P.IF[oy] * P.IF[oz], tgs[(t * F + f) * TXC + lane]);
+              bad |= !isfinite(v);
+              if (active) dstt[obase + f * P.t_plane] = v;
+            }
+          }
+        }
+      }
+    }
     double* tmp = ro;
     ro = rn;
     rn = tmp;
@@ -292,17 +287,17 @@ double host_fact(int k) {
   return r;
 }
 
-template <int MM, int NT, int CSOLE>
+template <int MM, int NT>
 int launch_one(const TParams& T, cudaStream_t st) {
   using G = Cfg<MM>;
-  const size_t smem = sizeof(double) * G::SMEM_DOUBLES;
+  const size_t smem = sizeof(double) * G::template SMEM_DOUBLES<NT>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tiled3d<MM, NT, CSOLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(tiled3d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     configured = true;
   }
   dim3 grid((T.tNx + TXC - 1) / TXC, T.tNy, (T.tNz + ZC - 1) / ZC);
-  tiled3d<MM, NT, CSOLE><<<grid, NTHREADS, smem, st>>>(T);
+  tiled3d<MM, NT><<<grid, NTHREADS, smem, st>>>(T);
   return 1;
 }
 
@@ -319,6 +314,7 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
         const int k = b0 + b1 + b2;
         T.GM[bindex(b0, b1, b2, MM)] = p.G[k] * host_fact(k) / (host_fact(b0) * host_fact(b1) * host_fact(b2));
       }
+  for (int o = 0; o <= MM; ++o) T.IF[o] = 1.0 / host_fact(o);
   T.s_layer = p.s_layer;
   T.s_plane = p.s_coef;
   T.t_layer = p.t_layer;
@@ -340,7 +336,7 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
     T.comp = 0;
     T.src = p.src[0];
     for (int t = 0; t < 3; ++t) T.dst[t] = p.dst[t];
-    return launch_one<MM, 3, 0>(T, st);
+    return launch_one<MM, 3>(T, st);
   }
   T.pre = 1;
   int launched = 0;
@@ -348,9 +344,7 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
     T.comp = c;
     T.src = p.src[c];
     T.dst[0] = p.dst[0];
-    if (c == 0) launched += launch_one<MM, 1, 0>(T, st);
-    else if (c == 1) launched += launch_one<MM, 1, 1>(T, st);
-    else launched += launch_one<MM, 1, 2>(T, st);
+    launched += launch_one<MM, 1>(T, st);
   }
   return launched;
 }

@@ -1,26 +1,31 @@
-"""Generate paper_1808_10481_b200/csrc/tiled3d_gen.cuh: straight-line Z-stage +
-Cauchy-Kowalewski code for every parity class of the tiled 3D kernel.
+"""Generate paper_1808_10481_b200/csrc/tiled3d_gen.cuh: straight-line stage code
+for the tiled 3D kernel (kernels_tiled3d.cu), for m = 1, 2, 3.
 
-Why generated: the class bodies are ~400 FMAs with compile-time operand
-indices.  Expressing them as templates/unrolled loop nests made nvcc's
-optimizer run for tens of minutes; explicit statements compile in seconds.
+Why generated: the stage bodies are hundreds of FMAs with compile-time operand
+indices.  Expressed as templates/unrolled loop nests they made nvcc's optimizer
+run for tens of minutes; explicit statements compile in seconds.  The code is
+also organised to keep the hot instruction footprint small (the first version
+specialised everything per parity class and ran out of instruction cache):
 
-Math (with rows of M pre-scaled by s!):
-  P~[qx,qy,qz] = qx! qy! qz! P[qx,qy,qz]
-  out_t[o] = (1/o!) sum_{|b|<=m} GM[b] P~[o + 2b + e_C(t)],   GM[b] = G_{|b|} |b|!/b!
-  target_t[o] += out_t[o]
-The z line of column (qx, qy) uses the parity split of M:
-  P~[qz] = sum_{l = qz mod 2} ML[qz][l] (L_l + R_l) - sum_{l != qz mod 2} ML[qz][l] (R_l - L_l)
-with L = ring_old (source layer k), R = ring_new (layer k+1).
+  m{m}_xy_px{p}   fused X+Y stage of one (l_z, q_x parity) task: 2(m+1) half
+                  x-lines (outputs q_x = p mod 2) feeding the y-lines in registers
+  m{m}_z_pz{p}    z stage of one parity class: P~[q] for the class's columns
+  m{m}_ck_*       closed-form CK sum of one target component in class-local
+                  indices (deduplicated: for odd m it depends only on the shift
+                  of the derivative axis, so 6 bodies serve all 24 (class, c))
 
-Usage: python tools/gen_tiled3d.py  (writes the header; committed)
+Math (rows of M pre-scaled by s!):
+  P~[q] = qx! qy! qz! P[q];  parity split of every 1D line:
+  out[s] = sum_{l = s mod 2} ML[s][l] (L_l + R_l) - sum_{l != s mod 2} ML[s][l] (R_l - L_l)
+  out_c[o] = (1/o!) sum_{|b| <= m} GM[b] P~[o + 2b + e_c],  GM[b] = G_|b| |b|!/b!
+Usage: python tools/gen_tiled3d.py   (writes the header; committed)
 """
 from __future__ import annotations
 
 import os
-from math import factorial
 
 TXC = 32
+RAWX = TXC + 1
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(HERE, "..", "paper_1808_10481_b200", "csrc", "tiled3d_gen.cuh")
 
@@ -36,95 +41,155 @@ def bindex(b, mm):
     raise ValueError(b)
 
 
-def gen_class(mm: int, comps: list[int], w: int, name: str) -> str:
+def half_line(mm, srcL, srcR, outs, tmp, lines):
+    """outputs s in `outs` of a parity-split line from L/R expressions."""
+    n1 = mm + 1
+    need_s, need_d = set(), set()
+    for s in outs:
+        for l in range(n1):
+            (need_s if (s + l) % 2 == 0 else need_d).add(l)
+    for l in sorted(need_s):
+        lines.append(f"  const double {tmp}s{l} = {srcL(l)} + {srcR(l)};")
+    for l in sorted(need_d):
+        lines.append(f"  const double {tmp}d{l} = {srcR(l)} - {srcL(l)};")
+    res = {}
+    for s in outs:
+        expr = "0.0"
+        for l in range(n1):
+            if (s + l) % 2 == 0:
+                expr = f"fma(P.ML[{s * n1 + l}], {tmp}s{l}, {expr})"
+            else:
+                expr = f"fma(-P.ML[{s * n1 + l}], {tmp}d{l}, {expr})"
+        name = f"{tmp}o{s}"
+        lines.append(f"  const double {name} = {expr};")
+        res[s] = name
+    return res
+
+
+def gen_xy(mm, px):
     n1, n = mm + 1, 2 * mm + 2
-    nh = n // 2
-    PX, PY, PZ = (w >> 2) & 1, (w >> 1) & 1, w & 1
-    L = []
-    L.append(f"__device__ __forceinline__ void {name}(const TParams& P, const double* __restrict__ ro,")
-    L.append("    const double* __restrict__ rn, int lane, double* const* dptr, bool active, bool& bad) {")
-    outs = []  # (t, C, (ox, oy, oz))
-    for t, C in enumerate(comps):
-        e = [int(C == a) for a in range(3)]
-        for ox in range(n1):
-            for oy in range(n1):
-                for oz in range(n1):
-                    if ((ox + e[0]) & 1, (oy + e[1]) & 1, (oz + e[2]) & 1) == (PX, PY, PZ):
-                        outs.append((t, C, (ox, oy, oz)))
-    # prefetch targets, zero accumulators
-    for i, (t, C, o) in enumerate(outs):
-        f = (o[0] * n1 + o[1]) * n1 + o[2]
-        L.append(f"  const double g{i} = active ? dptr[{t}][{f} * P.t_plane] : 0.0;")
-        L.append(f"  double a{i} = 0.0;")
-    for ix in range(nh):
-        qx = PX + 2 * ix
-        for iy in range(nh):
-            qy = PY + 2 * iy
-            L.append("  {")
-            base = (qx * n + qy) * n1
-            for l in range(n1):
-                L.append(f"    const double L{l} = ro[{(base + l) * TXC} + lane], R{l} = rn[{(base + l) * TXC} + lane];")
-            for l in range(n1):
-                if (l ^ PZ) & 1 == 0:
-                    L.append(f"    const double s{l} = L{l} + R{l};")
-                else:
-                    L.append(f"    const double d{l} = R{l} - L{l};")
-            for iz in range(nh):
-                s = PZ + 2 * iz
-                expr = "0.0"
-                for l in range(n1):
-                    if (s + l) & 1 == 0:
-                        expr = f"fma(P.ML[{s * n1 + l}], s{l}, {expr})"
-                    else:
-                        expr = f"fma(-P.ML[{s * n1 + l}], d{l}, {expr})"
-                L.append(f"    const double p{iz} = {expr};")
-            # CK terms landing in this column
-            for i, (t, C, o) in enumerate(outs):
-                e = [int(C == a) for a in range(3)]
-                for b0 in range(mm + 1):
-                    if o[0] + 2 * b0 + e[0] != qx:
-                        continue
-                    for b1 in range(mm + 1 - b0):
-                        if o[1] + 2 * b1 + e[1] != qy:
-                            continue
-                        for b2 in range(mm + 1 - b0 - b1):
-                            qz = o[2] + 2 * b2 + e[2]
-                            if qz >= n:
-                                continue
-                            bi = bindex((b0, b1, b2), mm)
-                            L.append(f"    a{i} = fma(P.GM[{bi}], p{(qz - PZ) // 2}, a{i});")
-            L.append("  }")
-    for i, (t, C, o) in enumerate(outs):
-        f = (o[0] * n1 + o[1]) * n1 + o[2]
-        inv = 1.0 / (factorial(o[0]) * factorial(o[1]) * factorial(o[2]))
-        L.append(f"  {{ const double v = fma(a{i}, {inv!r}, g{i}); bad |= !isfinite(v);"
-                 f" if (active) dptr[{t}][{f} * P.t_plane] = v; }}")
+    L = [f"__device__ __forceinline__ void m{mm}_xy_px{px}(const TParams& P, const double* __restrict__ rb,",
+         "                                                  double* __restrict__ wb) {",
+         "  // rb = raw + l_z*2*RAWX + lane;  wb = ring_new + l_z*TXC + lane"]
+    qxs = [q for q in range(n) if q % 2 == px]
+    xh = {}
+    for sy in range(2):
+        for ly in range(n1):
+            def off(lx, side, sy=sy, ly=ly):
+                return f"rb[{((lx * n1 * n1 + ly * n1) * 2 + sy) * RAWX + side}]"
+            res = half_line(mm, lambda l: off(l, 0), lambda l: off(l, 1), qxs, f"x{sy}{ly}", L)
+            for q, nm in res.items():
+                xh[(sy, ly, q)] = nm
+    for qx in qxs:
+        res = half_line(mm, lambda l, qx=qx: xh[(0, l, qx)], lambda l, qx=qx: xh[(1, l, qx)],
+                        list(range(n)), f"y{qx}", L)
+        for qy, nm in res.items():
+            L.append(f"  wb[{(qx * n + qy) * n1 * TXC}] = {nm};")
     L.append("}")
     return "\n".join(L)
 
 
+def gen_z(mm, pz):
+    n1, n = mm + 1, 2 * mm + 2
+    nh = n // 2
+    L = [f"__device__ __forceinline__ void m{mm}_z_pz{pz}(const TParams& P, const double* __restrict__ ro,",
+         f"    const double* __restrict__ rn, double (&pt)[{nh}][{nh}][{nh}]) {{",
+         "  // ro/rn = ring + ((PX*n + PY)*n1)*TXC + lane"]
+    for ix in range(nh):
+        for iy in range(nh):
+            off = ((2 * ix) * n + 2 * iy) * n1 * TXC
+            L.append("  {")
+            sub = []
+            res = half_line(mm, lambda l, off=off: f"ro[{off + l * TXC}]", lambda l, off=off: f"rn[{off + l * TXC}]",
+                            [pz + 2 * iz for iz in range(nh)], "z", sub)
+            L.extend("  " + s for s in sub)
+            for iz in range(nh):
+                L.append(f"    pt[{ix}][{iy}][{iz}] = {res[pz + 2 * iz]};")
+            L.append("  }")
+    L.append("}")
+    return "\n".join(L)
+
+
+def ck_body(mm, c, cls):
+    """CK for target component c in parity class cls = (PX, PY, PZ); returns
+    (list of (jx, jy, jz) outputs, list of statements)."""
+    n1, n = mm + 1, 2 * mm + 2
+    nh = n // 2
+    P = cls
+    e = [int(c == a) for a in range(3)]
+    outs = []
+    for ox in range(n1):
+        for oy in range(n1):
+            for oz in range(n1):
+                o = (ox, oy, oz)
+                if all(((o[a] + e[a]) & 1) == P[a] for a in range(3)):
+                    outs.append(o)
+    stm = []
+    for o in outs:
+        j = tuple((o[a] - ((P[a] - e[a]) & 1)) // 2 for a in range(3))
+        terms = []
+        for b0 in range(mm + 1):
+            for b1 in range(mm + 1 - b0):
+                for b2 in range(mm + 1 - b0 - b1):
+                    b = (b0, b1, b2)
+                    q = [o[a] + 2 * b[a] + e[a] for a in range(3)]
+                    if any(x >= n for x in q):
+                        continue
+                    i = tuple((q[a] - P[a]) // 2 for a in range(3))
+                    terms.append((bindex(b, mm), i))
+        for bi, i in terms:
+            stm.append(f"  acc[{j[0]}][{j[1]}][{j[2]}] = fma(P.GM[{bi}], pt[{i[0]}][{i[1]}][{i[2]}], acc[{j[0]}][{j[1]}][{j[2]}]);")
+    return outs, stm
+
+
 def main():
-    parts = [
-        "// GENERATED by tools/gen_tiled3d.py -- do not edit.",
-        "// Z-stage + closed-form CK per parity class for kernels_tiled3d.cu.",
-        "#pragma once",
-        "",
-    ]
+    parts = ["// GENERATED by tools/gen_tiled3d.py -- do not edit.",
+             "// Stage code of the tiled 3D Hermite-leapfrog kernel (kernels_tiled3d.cu).",
+             "#pragma once", ""]
     for mm in (1, 2, 3):
-        kinds = [("vel", [0, 1, 2])] + [(f"pre{c}", [c]) for c in range(3)]
-        for kname, comps in kinds:
-            for w in range(8):
-                parts.append(gen_class(mm, comps, w, f"zck_m{mm}_{kname}_{w}"))
-                parts.append("")
-            parts.append(f"__device__ __forceinline__ void zck_m{mm}_{kname}(int w, const TParams& P, const double* ro,")
-            parts.append("    const double* rn, int lane, double* const* dptr, bool active, bool& bad) {")
-            parts.append("  switch (w) {")
-            for w in range(8):
-                parts.append(f"    case {w}: zck_m{mm}_{kname}_{w}(P, ro, rn, lane, dptr, active, bad); break;")
-            parts.append("    default: break;")
-            parts.append("  }")
-            parts.append("}")
+        n1, n = mm + 1, 2 * mm + 2
+        nh, jh = n // 2, (n1 + 1) // 2
+        parts.append(f"// ---------------- m = {mm}")
+        for px in range(2):
+            parts.append(gen_xy(mm, px))
             parts.append("")
+        for pz in range(2):
+            parts.append(gen_z(mm, pz))
+            parts.append("")
+        bodies = {}
+        dispatch = {}
+        for c in range(3):
+            for w in range(8):
+                cls = ((w >> 2) & 1, (w >> 1) & 1, w & 1)
+                outs, stm = ck_body(mm, c, cls)
+                key = "\n".join(stm)
+                if key not in bodies:
+                    fname = f"m{mm}_ck_{len(bodies)}"
+                    bodies[key] = fname
+                    parts.append(f"__device__ __forceinline__ void {fname}(const TParams& P, const double (&pt)[{nh}][{nh}][{nh}],")
+                    parts.append(f"    double (&acc)[{jh}][{jh}][{jh}]) {{")
+                    parts.extend(stm)
+                    parts.append("}")
+                    parts.append("")
+                dispatch[(c, w)] = bodies[key]
+        parts.append(f"__device__ __forceinline__ void m{mm}_ck(int c, int w, const TParams& P,")
+        parts.append(f"    const double (&pt)[{nh}][{nh}][{nh}], double (&acc)[{jh}][{jh}][{jh}]) {{")
+        # group (c, w) by body to keep the dispatch small
+        by_body = {}
+        for (c, w), fn in dispatch.items():
+            by_body.setdefault(fn, []).append(c * 8 + w)
+        parts.append("  switch (c * 8 + w) {")
+        for fn, keys in by_body.items():
+            for k in keys:
+                parts.append(f"    case {k}:")
+            parts.append(f"      {fn}(P, pt, acc);")
+            parts.append("      break;")
+        parts.append("    default: break;")
+        parts.append("  }")
+        parts.append("}")
+        parts.append("")
+        parts.append(f"// m = {mm}: {len(bodies)} distinct CK bodies")
+        parts.append("")
     with open(OUT, "w") as f:
         f.write("\n".join(parts))
     print("wrote", OUT)

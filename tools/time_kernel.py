@@ -5,11 +5,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1808_10481_b200 as H
 
-d, m, K = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+d, m = int(sys.argv[1]), int(sys.argv[2])
+Ks = [int(x) for x in sys.argv[3].split("x")]
+Ks = Ks if len(Ks) == d else Ks * d
+K = Ks[0]
 steps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 variant = int(sys.argv[5]) if len(sys.argv) > 5 else -1
 stream = torch.cuda.Stream()
-Ks = [K] * d
 g = H.Stepper(H.Grid([-1.0] * d, 2.0 / K, tuple(Ks)), m, stream=stream.cuda_stream)
 if variant >= 0:
     g.kernel_variant = variant
@@ -26,5 +28,5 @@ g.advance_n(steps)
 e1.record(stream)
 e1.synchronize()
 ms = e0.elapsed_time(e1) / steps
-dof = (d + 1) * (m + 1) ** d * K ** d
-print(f"d={d} m={m} K={K} variant={g.kernel_variant} ms/step={ms:.3f} DOF/s={dof / ms * 1e3:.3e} GB/s(24B/DOF)={24 * dof / ms / 1e6:.1f}")
+dof = (d + 1) * (m + 1) ** d * math.prod(Ks)
+print(f"d={d} m={m} K={Ks} variant={g.kernel_variant} ms/step={ms:.3f} DOF/s={dof / ms * 1e3:.3e} GB/s(24B/DOF)={24 * dof / ms / 1e6:.1f}")
