@@ -99,6 +99,10 @@ hlf_status hlf_set_dt(hlf_solver* s, double dt);
 /* --- stepping (asynchronous on the solver's stream) ---------------------- */
 hlf_status hlf_advance_p(hlf_solver* s);
 hlf_status hlf_advance_v(hlf_solver* s);
+/* the same half steps recording non-finite values under step_index (no sync);
+   for callers that interleave halo exchanges (z slabs) */
+hlf_status hlf_advance_p_indexed(hlf_solver* s, int step_index);
+hlf_status hlf_advance_v_indexed(hlf_solver* s, int step_index);
 /* advance_p, advance_v, finite check: HLF_INSTABILITY (synchronous) if the
    state became non-finite; message "solution became non-finite at step N" */
 hlf_status hlf_step(hlf_solver* s, int step_index);

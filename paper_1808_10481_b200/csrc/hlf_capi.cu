@@ -479,6 +479,26 @@ hlf_status hlf_advance_v(hlf_solver* s) {
   return HLF_OK;
 }
 
+hlf_status hlf_advance_p_indexed(hlf_solver* s, int step_index) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (s->variable && !s->coeff[HLF_PRIMARY]) return fail(s, HLF_CONFIG_ERROR, "primary-grid ap jets not set");
+  cudaSetDevice(s->device);
+  hlf_status st = launch_half(s, hlfk::PRE, step_index);
+  if (st != HLF_OK) return st;
+  s->t_p += s->dt;
+  return HLF_OK;
+}
+
+hlf_status hlf_advance_v_indexed(hlf_solver* s, int step_index) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (s->variable && !s->coeff[HLF_DUAL]) return fail(s, HLF_CONFIG_ERROR, "dual-grid ap jets not set");
+  cudaSetDevice(s->device);
+  hlf_status st = launch_half(s, hlfk::VEL, step_index);
+  if (st != HLF_OK) return st;
+  s->t_v += s->dt;
+  return HLF_OK;
+}
+
 static hlf_status step_async(hlf_solver* s, int step_index) {
   if (s->variable && (!s->coeff[0] || !s->coeff[1])) return fail(s, HLF_CONFIG_ERROR, "ap jets not set");
   hlf_status st = launch_half(s, hlfk::PRE, step_index);

@@ -1,0 +1,191 @@
+"""z-slab domain decomposition of the 3D Hermite-leapfrog step across GPUs.
+
+One process per GPU (torch.distributed, NCCL).  Rank r owns cells
+z in [r Kz, (r+1) Kz) of a periodic domain:
+  * before advance_p (pressure half step) it needs the dual v layer z = -1,
+    i.e. the previous rank's last v layer  -> v halo, 3 components;
+  * before advance_v (velocity half step) it needs the primary p layer z = Kz,
+    i.e. the next rank's first p layer      -> p halo.
+A layer of one field is contiguous in the SoA layout [layer][coef][y][x], so
+each halo is one NCCL send/recv of the layer with no packing.  The halos
+land directly in the solver's ghost layers (hlf_halo_recv_ptr).  The exchange
+is issued on the solver's stream; with one rank the library wraps z itself.
+
+The exchange logic only needs a backend with advance_p_indexed,
+advance_v_indexed and halo views; `Stepper` (CUDA) is the product backend,
+the tests drive the same logic over gloo with a CPU backend.
+"""
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+
+from .solver import Grid, Stepper
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of solver-owned device memory."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr: int, count: int):
+    import torch
+    return torch.as_tensor(_DevArray(ptr, count), device="cuda")
+
+
+class HaloExchanger:
+    """Pairs the z halo sends/receives of one slab with its ring neighbours."""
+
+    def __init__(self, backend, rank: int, world: int, views):
+        """views(kind, comp, send) -> tensor over the halo layer."""
+        self.rank, self.world = rank, world
+        self.prev = (rank - 1) % world
+        self.next = (rank + 1) % world
+        self.p_send = views(0, 0, True)
+        self.p_recv = views(0, 0, False)
+        self.v_send = [views(1, c, True) for c in range(3)]
+        self.v_recv = [views(1, c, False) for c in range(3)]
+
+    def _run(self, ops):
+        import torch.distributed as dist
+        reqs = dist.batch_isend_irecv(ops)
+        for r in reqs:
+            r.wait()
+
+    def exchange_p(self):
+        # my p layer 0 is the previous rank's layer Kz; my layer Kz comes from the next rank
+        import torch.distributed as dist
+        self._run([dist.P2POp(dist.isend, self.p_send, self.prev),
+                   dist.P2POp(dist.irecv, self.p_recv, self.next)])
+
+    def exchange_v(self):
+        # my last v layer is the next rank's ghost z = -1; my ghost comes from the previous rank
+        import torch.distributed as dist
+        ops = []
+        for c in range(3):
+            ops.append(dist.P2POp(dist.isend, self.v_send[c], self.next))
+            ops.append(dist.P2POp(dist.irecv, self.v_recv[c], self.prev))
+        self._run(ops)
+
+
+class SlabStepper:
+    """3D acoustic stepper on one z-slab of a periodic box (one rank per GPU)."""
+
+    def __init__(self, K_global, h: float, m: int, rank: int = 0, world: int = 1, device: int = 0,
+                 stream=None, x_min=(-1.0, -1.0, -1.0)):
+        Kx, Ky, Kz = K_global
+        if Kz % world:
+            raise ValueError("global z cells must divide evenly across ranks")
+        self.K_global = tuple(K_global)
+        self.kz = Kz // world
+        self.rank, self.world = rank, world
+        self.m, self.h = m, h
+        self.stream = stream
+        x0 = (x_min[0], x_min[1], x_min[2] + rank * self.kz * h)
+        grid = Grid(x0, h, (Kx, Ky, self.kz))
+        sptr = stream.cuda_stream if stream is not None else None
+        self.solver = Stepper(grid, m, device=device, stream=sptr, z_slab=world > 1)
+        self.halo = None
+        if world > 1:
+            def views(kind, comp, send):
+                ptr, cnt = self.solver.halo_ptr(kind, comp, send)
+                return device_view(ptr, cnt)
+            self.halo = HaloExchanger(self.solver, rank, world, views)
+
+    # ---- data
+    def init_mode(self, cfl: float = 0.9, t0: float = 0.0):
+        """Standing mode p = sin(pi x) sin(pi y) sin(pi z) cos(sqrt(3) pi t) on
+        [-1, 1]^3 and its velocity v_c = -(1/sqrt 3) d_c(...) sin(sqrt(3) pi t)
+        at t0 + dt/2 (leapfrog staggering, stepper1d.cpp:131-145), exact jets on
+        the device; dt = cfl h / sqrt(3)."""
+        s = self.solver
+        pi = math.pi
+        wt = math.sqrt(3.0) * pi
+        dt = cfl * self.h / math.sqrt(3.0)
+        tv = t0 + dt / 2
+        for f in range(4):
+            s.zero_field(f)
+        s.fill_separable(0, math.cos(wt * t0), [pi] * 3, [0.0] * 3)
+        for c in range(3):
+            ph = [pi / 2 if a == c else 0.0 for a in range(3)]
+            s.fill_separable(1 + c, -(pi / wt) * math.sin(wt * tv), [pi] * 3, ph)
+        s.set_times(t0, tv, dt)
+        return dt
+
+    # ---- stepping
+    def step(self, step_index: int):
+        s = self.solver
+        if self.halo:
+            self.halo.exchange_v()
+        s.advance_p_indexed(step_index)
+        if self.halo:
+            self.halo.exchange_p()
+        s.advance_v_indexed(step_index)
+
+    def launch_count(self) -> int:
+        return self.solver.launch_count
+
+    def poll_finite(self) -> int:
+        return self.solver.poll_finite()
+
+    def kernel_times(self, steps: int = 2):
+        """Device time of the pressure half step (3 launches) and the velocity
+        half step (1 launch), CUDA events on the solver stream."""
+        import torch
+        st = self.stream or torch.cuda.current_stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        pre = vel = 0.0
+        for i in range(steps):
+            if self.halo:
+                self.halo.exchange_v()
+            ev[0].record(st)
+            self.solver.advance_p_indexed(-1)
+            ev[1].record(st)
+            if self.halo:
+                self.halo.exchange_p()
+                ev[1].record(st)
+            self.solver.advance_v_indexed(-1)
+            ev[2].record(st)
+            ev[2].synchronize()
+            pre += ev[0].elapsed_time(ev[1])
+            vel += ev[1].elapsed_time(ev[2])
+        return {"pre_ms": pre / steps, "pre_ms_per_launch": pre / steps / 3.0, "vel_ms": vel / steps}
+
+    def e2e(self, steps: int, dof_per_step: int):
+        """End to end through the C-ABI: upload the staggered state from pinned
+        host memory (hlf_set_field), advance `steps` leapfrog steps
+        (hlf_advance_n semantics: one finite check at the end), download it
+        (hlf_get_field).  Returns the e2e JSON object."""
+        import torch
+        s = self.solver
+        bufs = []
+        for f in range(4):
+            n = s.field_nodes(f) * s.F
+            bufs.append(torch.empty(n, dtype=torch.float64, pin_memory=True))
+        torch.cuda.synchronize()
+        for f in range(4):
+            s.get_field_ptr(f, bufs[f].data_ptr())  # a real state to upload
+        nbytes = sum(b.numel() * 8 for b in bufs)
+        t_p, t_v, dt = s.times()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for f in range(4):
+            s.set_field_ptr(f, bufs[f].data_ptr())
+        s.set_times(t_p, t_v, dt)
+        for i in range(steps):
+            self.step(i)
+        bad = s.poll_finite()
+        for f in range(4):
+            s.get_field_ptr(f, bufs[f].data_ptr())
+        sec = time.perf_counter() - t0
+        del bufs
+        return {"value": dof_per_step * steps / sec, "unit": "DOF-updates/s",
+                "h2d_bytes_per_step": nbytes / steps, "d2h_bytes_per_step": nbytes / steps,
+                "job": {"leapfrog_steps": steps, "h2d_bytes": nbytes, "d2h_bytes": nbytes, "seconds": sec,
+                        "api": "hlf_set_field x4 (pinned host AoS) + hlf_advance_p/v_indexed x steps + "
+                               "hlf_poll_finite + hlf_get_field x4, wall clock", "finite": bad < 0}}

@@ -304,6 +304,12 @@ class Stepper:
     def advance_v(self):
         self._c(self._L.hlf_advance_v(self._h))
 
+    def advance_p_indexed(self, step_index: int):
+        self._c(self._L.hlf_advance_p_indexed(self._h, step_index))
+
+    def advance_v_indexed(self, step_index: int):
+        self._c(self._L.hlf_advance_v_indexed(self._h, step_index))
+
     def step_system(self, step_index: int):
         self._c(self._L.hlf_step(self._h, step_index))
 
