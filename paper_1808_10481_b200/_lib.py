@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libhlf_b200.so")
+LIB_PATH = os.environ.get("HLF_B200_LIB_OVERRIDE") or os.path.join(HERE, "lib", "libhlf_b200.so")
 
 HLF_OK = 0
 HLF_CONFIG_ERROR = 1

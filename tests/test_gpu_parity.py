@@ -114,6 +114,24 @@ def test_parity_3d_tiled_kernel(m, boundary):
     compare(g, o, 3)
 
 
+def test_custom_M_falls_back_to_generic_kernel():
+    # the tiled kernel has M baked in; a caller-supplied M that differs must
+    # still be honoured (generic kernel), matching the oracle run with that M
+    m, K = 3, [18, 4, 5]
+    h = 2.0 / K[0]
+    M = H.build_interp_operator(m).M * (1.0 + 2.0 ** -40)
+    g = H.Stepper(H.Grid([-1.0] * 3, h, tuple(K)), m, M=M)
+    o = O.OracleStepper(3, m, K, h)
+    o.set_M(M)
+    rng = np.random.default_rng(4)
+    for f in range(4):
+        a = rng.standard_normal((g.field_nodes(f), g.F)) * 0.6 ** np.arange(g.F)
+        g.set_field(f, a)
+        o.set_field(f, a)
+    run_both(g, o, 2, 0.25 * h)
+    compare(g, o, 3)
+
+
 def test_tiled_equals_generic_long_run():
     # the tiled kernel reorders the arithmetic (parity split, FMA); over a long
     # run the two GPU kernels differ by the reconstruction's roundoff floor only
