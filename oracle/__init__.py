@@ -117,6 +117,9 @@ def orc_lib():
         L.orc_advance_n.argtypes = [C.c_void_p, C.c_int, C.c_int]
         L.orc_advance_n.restype = C.c_int
         L.orc_reconstruct.argtypes = [C.c_void_p, _dp, _dp]
+        L.orc_set_slab.argtypes = [C.c_void_p, C.c_int]
+        L.orc_get_layer.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp]
+        L.orc_set_halo.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp]
         L.orc_add_separable.argtypes = [C.c_int, _ip, _dp, C.c_double, C.c_double, C.c_int, C.c_double, _dp, _dp, _dp]
         _orc_lib = L
     return _orc_lib
@@ -319,6 +322,27 @@ class OracleStepper:
 
     def advance_n(self, n: int, first: int = 0) -> int:
         return self.L.orc_advance_n(self.h_, n, first)
+
+    # z-slab mode (tests of the multi-GPU halo logic on CPU)
+    def set_slab(self, on: bool = True):
+        self.L.orc_set_slab(self.h_, int(on))
+
+    def layer_size(self, field: int) -> int:
+        nx, ny = (self.num_nodes(0) if field == 0 else self.num_nodes(1)), 1
+        K = self.K
+        if field == 0:
+            Np = [k + 1 if b == 1 else k for k, b in zip(K, self.boundary)]
+            return Np[0] * Np[1] * self.F
+        return K[0] * K[1] * self.F
+
+    def get_layer(self, field: int, z: int) -> np.ndarray:
+        out = np.zeros(self.layer_size(field))
+        self.L.orc_get_layer(self.h_, field, z, _ptr(out))
+        return out
+
+    def set_halo(self, kind: int, comp: int, data):
+        a = np.ascontiguousarray(data, dtype=np.float64).ravel()
+        self.L.orc_set_halo(self.h_, kind, comp, _ptr(a))
 
     def reconstruct(self, corners) -> np.ndarray:
         c = np.ascontiguousarray(corners, dtype=np.float64).ravel()

@@ -106,6 +106,11 @@ struct Oracle {
   std::vector<double> p;            // [primary node][F]
   std::vector<double> v[3];         // [dual node][F]
   std::vector<double> cj[2][2];     // [grid][ap/av] per-node n^d jets (empty = constant)
+  // z-slab mode (d = 3, periodic z across ranks): z neighbours beyond the slab
+  // come from halo layers set by the caller, [ix][iy][F]
+  bool slab = false;
+  std::vector<double> p_halo;       // primary layer z = Kz (next rank's layer 0)
+  std::vector<double> v_halo[3];    // dual layer z = -1 (previous rank's layer Kz-1)
   double t_p = 0.0, t_v = 0.0, dt = 0.0;
 
   size_t nodes(int grid) const {
@@ -224,6 +229,14 @@ struct Oracle {
   // ghost handling for the dual (velocity) family: returns the jet to use for
   // dual index idx (may be -1 or K along reflective axes) of component comp
   void dual_jet(int comp, const int* idx_in, double* out) const {
+    if (slab && d == 3 && idx_in[2] < 0) {
+      int ix = idx_in[0] % K[0], iy = idx_in[1] % K[1];
+      ix = ix < 0 ? ix + K[0] : ix;
+      iy = iy < 0 ? iy + K[1] : iy;
+      const double* src = v_halo[comp].data() + (static_cast<size_t>(ix) * Nd[1] + iy) * F;
+      std::memcpy(out, src, sizeof(double) * F);
+      return;
+    }
     int idx[3] = {idx_in[0], idx_in[1], idx_in[2]};
     int flip[3] = {0, 0, 0};
     double sigma = 1.0;
@@ -318,12 +331,15 @@ struct Oracle {
       std::vector<const double*> cp(nc);
       for (int corner = 0; corner < nc; ++corner) {
         int pi[3] = {0, 0, 0};
+        bool halo = false;
         for (int ax = 0; ax < d; ++ax) {
           int q = idx[ax] + ((corner >> ax) & 1);
+          if (slab && ax == 2 && q == K[2]) halo = true;
           if (bnd[ax] == 0) q %= K[ax];
           pi[ax] = q;
         }
-        cp[corner] = p.data() + node_index(0, pi) * F;
+        cp[corner] = halo ? p_halo.data() + (static_cast<size_t>(pi[0]) * Np[1] + pi[1]) * F
+                          : p.data() + node_index(0, pi) * F;
       }
       std::vector<std::vector<double>> P(n, std::vector<double>(E, 0.0));
       std::vector<std::vector<double>> V[3];
@@ -449,6 +465,37 @@ int orc_advance_n(void* h, int nsteps, int first_step) {
     if (!o->all_finite()) return first_step + i;
   }
   return -1;
+}
+
+// z-slab mode: halos replace the periodic z wrap (d = 3)
+void orc_set_slab(void* h, int on) {
+  Oracle* o = static_cast<Oracle*>(h);
+  o->slab = on != 0;
+  const size_t plane_p = static_cast<size_t>(o->Np[0]) * o->Np[1] * o->F;
+  const size_t plane_d = static_cast<size_t>(o->Nd[0]) * o->Nd[1] * o->F;
+  o->p_halo.assign(plane_p, 0.0);
+  for (int c = 0; c < 3; ++c) o->v_halo[c].assign(plane_d, 0.0);
+}
+
+// copy z-layer z of a field out as [ix][iy][F]
+void orc_get_layer(void* h, int field, int z, double* out) {
+  Oracle* o = static_cast<Oracle*>(h);
+  const int grid = field == 0 ? 0 : 1;
+  const int* N = grid == 0 ? o->Np : o->Nd;
+  const std::vector<double>& src = field == 0 ? o->p : o->v[field - 1];
+  for (int ix = 0; ix < N[0]; ++ix)
+    for (int iy = 0; iy < N[1]; ++iy) {
+      const int idx[3] = {ix, iy, z};
+      std::memcpy(out + (static_cast<size_t>(ix) * N[1] + iy) * o->F, src.data() + o->node_index(grid, idx) * o->F,
+                  sizeof(double) * o->F);
+    }
+}
+
+// kind 0: p halo (layer Kz); kind 1: v halo of component comp (layer -1)
+void orc_set_halo(void* h, int kind, int comp, const double* in) {
+  Oracle* o = static_cast<Oracle*>(h);
+  std::vector<double>& dst = kind == 0 ? o->p_halo : o->v_halo[comp];
+  std::memcpy(dst.data(), in, sizeof(double) * dst.size());
 }
 
 // reconstruct one cell from 2^d corner jets (for direct reconstruction tests)

@@ -39,10 +39,14 @@ def device_view(ptr: int, count: int):
 
 
 class HaloExchanger:
-    """Pairs the z halo sends/receives of one slab with its ring neighbours."""
+    """Pairs the z halo sends/receives of one slab with its ring neighbours.
 
-    def __init__(self, backend, rank: int, world: int, views):
-        """views(kind, comp, send) -> tensor over the halo layer."""
+    `views(kind, comp, send)` returns the tensor a halo is sent from / received
+    into (kind 0 = p layer, 1 = v layer of component comp).  For the CUDA
+    backend the tensors alias the solver's own layers, so `pack`/`unpack` are
+    no-ops; a host backend may copy in `pack(kind)` / `unpack(kind)`."""
+
+    def __init__(self, rank: int, world: int, views, pack=None, unpack=None):
         self.rank, self.world = rank, world
         self.prev = (rank - 1) % world
         self.next = (rank + 1) % world
@@ -50,6 +54,8 @@ class HaloExchanger:
         self.p_recv = views(0, 0, False)
         self.v_send = [views(1, c, True) for c in range(3)]
         self.v_recv = [views(1, c, False) for c in range(3)]
+        self.pack = pack or (lambda kind: None)
+        self.unpack = unpack or (lambda kind: None)
 
     def _run(self, ops):
         import torch.distributed as dist
@@ -60,17 +66,32 @@ class HaloExchanger:
     def exchange_p(self):
         # my p layer 0 is the previous rank's layer Kz; my layer Kz comes from the next rank
         import torch.distributed as dist
+        self.pack(0)
         self._run([dist.P2POp(dist.isend, self.p_send, self.prev),
                    dist.P2POp(dist.irecv, self.p_recv, self.next)])
+        self.unpack(0)
 
     def exchange_v(self):
         # my last v layer is the next rank's ghost z = -1; my ghost comes from the previous rank
         import torch.distributed as dist
+        self.pack(1)
         ops = []
         for c in range(3):
             ops.append(dist.P2POp(dist.isend, self.v_send[c], self.next))
             ops.append(dist.P2POp(dist.irecv, self.v_recv[c], self.prev))
         self._run(ops)
+        self.unpack(1)
+
+
+def slab_step(solver, halo, step_index: int):
+    """One full leapfrog step of a slab (step_system order, stepper1d.cpp:168-172):
+    v halo -> advance_p -> p halo -> advance_v."""
+    if halo:
+        halo.exchange_v()
+    solver.advance_p_indexed(step_index)
+    if halo:
+        halo.exchange_p()
+    solver.advance_v_indexed(step_index)
 
 
 class SlabStepper:
@@ -95,7 +116,7 @@ class SlabStepper:
             def views(kind, comp, send):
                 ptr, cnt = self.solver.halo_ptr(kind, comp, send)
                 return device_view(ptr, cnt)
-            self.halo = HaloExchanger(self.solver, rank, world, views)
+            self.halo = HaloExchanger(rank, world, views)
 
     # ---- data
     def init_mode(self, cfl: float = 0.9, t0: float = 0.0):
@@ -119,13 +140,7 @@ class SlabStepper:
 
     # ---- stepping
     def step(self, step_index: int):
-        s = self.solver
-        if self.halo:
-            self.halo.exchange_v()
-        s.advance_p_indexed(step_index)
-        if self.halo:
-            self.halo.exchange_p()
-        s.advance_v_indexed(step_index)
+        slab_step(self.solver, self.halo, step_index)
 
     def launch_count(self) -> int:
         return self.solver.launch_count

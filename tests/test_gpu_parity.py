@@ -290,3 +290,56 @@ def test_advance_n_equals_step_loop():
         gb.step_system(3 + i)
     for f in range(3):
         assert np.array_equal(ga.get_field(f), gb.get_field(f))
+
+
+@pytest.mark.parametrize("m", [1, 3])
+def test_z_slabs_on_one_gpu_match_single_domain(m):
+    """Two z-slab solvers (z_slab=True) on one GPU, halos copied through the
+    hlf_halo_send/recv_ptr device views exactly as the NCCL exchanger does;
+    the result equals one periodic solver on the whole box."""
+    import torch
+    from paper_1808_10481_b200.distributed import device_view
+    K = [36, 4, 8]
+    h = 2.0 / K[0]
+    full = H.Stepper(H.Grid([-1.0] * 3, h, tuple(K)), m)
+    kz = K[2] // 2
+    slabs = [H.Stepper(H.Grid([-1.0, -1.0, -1.0 + r * kz * h], h, (K[0], K[1], kz)), m, z_slab=True)
+             for r in range(2)]
+    rng = np.random.default_rng(8)
+    F = (m + 1) ** 3
+    for f in range(4):
+        a = rng.standard_normal((K[0] * K[1] * K[2], F)) * 0.6 ** np.arange(F)
+        full.set_field(f, a)
+        a4 = a.reshape(K[0], K[1], K[2], F)
+        for r in range(2):
+            slabs[r].set_field(f, a4[:, :, r * kz:(r + 1) * kz, :].reshape(-1, F))
+    dt = 0.25 * h
+    for s in [full] + slabs:
+        s.set_times(0.0, dt / 2, dt)
+
+    def view(s, kind, comp, send):
+        ptr, cnt = s.halo_ptr(kind, comp, send)
+        return device_view(ptr, cnt)
+
+    for i in range(3):
+        for s in slabs:
+            s.synchronize()
+        for r in range(2):  # v halo: my ghost z=-1 <- previous rank's last layer
+            for c in range(3):
+                view(slabs[r], 1, c, False).copy_(view(slabs[(r - 1) % 2], 1, c, True))
+        torch.cuda.synchronize()
+        for s in slabs:
+            s.advance_p_indexed(i)
+            s.synchronize()
+        for r in range(2):  # p halo: my layer Kz <- next rank's layer 0
+            view(slabs[r], 0, 0, False).copy_(view(slabs[(r + 1) % 2], 0, 0, True))
+        torch.cuda.synchronize()
+        for s in slabs:
+            s.advance_v_indexed(i)
+            s.synchronize()
+        full.step_system(i)
+    for f in range(4):
+        ref = full.get_field(f).reshape(K[0], K[1], K[2], F)
+        for r in range(2):
+            got = slabs[r].get_field(f).reshape(K[0], K[1], kz, F)
+            assert np.array_equal(got, ref[:, :, r * kz:(r + 1) * kz, :]), (f, r)
