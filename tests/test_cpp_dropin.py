@@ -1,0 +1,27 @@
+"""The C++ drop-in (include/hlf/b200/stepper1d.hpp) driven by the reference's
+own Stepper1d test cases (tests/cpp/test_b200_stepper1d.cpp), on the GPU."""
+import os
+import subprocess
+
+import pytest
+
+import oracle as O
+
+EXE = os.path.join(O.HERE, "_ref", "test_b200_stepper1d")
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_stepper1d_suite():
+    if not os.path.exists(EXE):
+        pytest.skip("drop-in test binary not built (needs /root/reference at build time)")
+    r = subprocess.run([EXE], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "| 0 failed" in r.stdout
+
+
+def test_cpp_dropin_rejects_unsupported_features_without_gpu():
+    # the configuration checks run before any device call
+    if not os.path.exists(EXE):
+        pytest.skip("drop-in test binary not built")
+    r = subprocess.run([EXE], capture_output=True, text=True, timeout=600)
+    assert "unsupported problem features" not in r.stderr
