@@ -62,6 +62,10 @@ int launch_half_generic(int d, int m, bool variable, HalfKind kind, const HalfPa
 int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
 bool tiled3d_supported(int m);
 int launch_fill(const FillParams& p, cudaStream_t st);
+namespace v5 {
+// 16-warp tiled kernel, m = 3 (kernels_tiled3d_v5.cu)
+int launch(HalfKind kind, const HalfParams& p, cudaStream_t st);
+}
 // z ghost mirror for the dual family: dst layer = sign * (-1)^{c_z} src layer
 int launch_mirror_layer(double* dst, const double* src, int64_t plane, int n1, int d, double sigma,
                         cudaStream_t st);

@@ -24,6 +24,7 @@
 // VEL (p -> v_x, v_y, v_z) is one launch; PRE (v -> p) is three launches, one
 // per source component c, each adding the c-th divergence term (q_c+1)V_c[q+e_c]
 // through the same code with target component c.
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <utility>
@@ -98,15 +99,6 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #include "tiled3d_gen.cuh"
 
 template <int MM>
-__device__ __forceinline__ void issue_raw(double* raw, const double* base, const int* off, int tid) {
-  using G = Cfg<MM>;
-#pragma unroll
-  for (int t = 0; t < G::RAW_PER_THREAD; ++t)
-    if (off[t] >= 0) cp_async8(raw + tid + t * NTHREADS, base + off[t]);
-  cp_async_commit();
-}
-
-template <int MM>
 __device__ __forceinline__ void xy_task(const TParams& P, int w, const double* raw, double* rn, int lane) {
   // task w = (l_z, q_x parity): fused X+Y stage into the ring layer rn
   constexpr int n1 = MM + 1;
@@ -162,49 +154,88 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
   if (k0 >= k1) return;
   const bool active = x0 + lane < P.tNx;
 
-  // per-thread raw-element offsets (the same for every layer) and mirror signs
-  int off[G::RAW_PER_THREAD];
-  unsigned negmask = 0;
-#pragma unroll 1
-  for (int t = 0; t < G::RAW_PER_THREAD; ++t) {
-    const int e = tid + t * NTHREADS;
-    off[t] = -1;
-    if (e >= G::RAW) continue;
-    const int f = e / (2 * RAWX);
-    const int r = e - f * 2 * RAWX;
-    const int sy = r / RAWX, sx = r - sy * RAWX;
-    int q0 = x0 + sx - P.pre, q1 = ty + sy - P.pre;
-    bool neg = false;
-    const int ax0 = f / (n1 * n1), ay0 = (f / n1) % n1;
+  // Raw layer = 2 F rows (f, source row sy) of RAWX nodes; warp w streams rows
+  // w, w+8, ... with lane = node sx (sx = 32 of every row by thread tid < 2F).
+  // The x/y node maps (wrap, or mirror at walls) are the same for every row
+  // and layer, so they are computed once.
+  auto xmap = [&](int sx, bool& mir) {
+    int q = x0 + sx - P.pre;
+    mir = false;
     if (P.bnd[0] == 0) {
-      if (q0 >= P.K[0]) q0 -= P.K[0];
-      if (q0 < 0) q0 += P.K[0];
-    } else if (P.pre && (q0 < 0 || q0 == P.K[0])) {
-      q0 = q0 < 0 ? 0 : P.K[0] - 1;
-      neg ^= (ax0 & 1) != 0;
-      neg ^= P.comp != 0;
+      if (q >= P.K[0]) q -= P.K[0];
+      if (q < 0) q += P.K[0];
+    } else if (P.pre && (q < 0 || q == P.K[0])) {
+      q = q < 0 ? 0 : P.K[0] - 1;
+      mir = true;
     }
-    if (q0 >= P.sNx) q0 = P.sNx - 1;
+    return q >= P.sNx ? P.sNx - 1 : q;
+  };
+  auto ymap = [&](int sy, bool& mir) {
+    int q = ty + sy - P.pre;
+    mir = false;
     if (P.bnd[1] == 0) {
-      if (q1 >= P.K[1]) q1 -= P.K[1];
-      if (q1 < 0) q1 += P.K[1];
-    } else if (P.pre && (q1 < 0 || q1 == P.K[1])) {
-      q1 = q1 < 0 ? 0 : P.K[1] - 1;
-      neg ^= (ay0 & 1) != 0;
-      neg ^= P.comp != 1;
+      if (q >= P.K[1]) q -= P.K[1];
+      if (q < 0) q += P.K[1];
+    } else if (P.pre && (q < 0 || q == P.K[1])) {
+      q = q < 0 ? 0 : P.K[1] - 1;
+      mir = true;
     }
-    if (q1 >= P.sNy) q1 = P.sNy - 1;
-    off[t] = static_cast<int>(f * P.s_plane + static_cast<int64_t>(q1) * P.sNx + q0);
-    if (neg) negmask |= 1u << t;
-  }
-  auto finish_raw = [&]() {  // (tiny; kept inline)
+    return q >= P.sNy ? P.sNy - 1 : q;
+  };
+  bool mx_lane, mx_last, my0, my1;
+  const int xo_lane = xmap(lane, mx_lane);
+  const int xo_last = xmap(TXC, mx_last);
+  const int64_t yo0 = static_cast<int64_t>(ymap(0, my0)) * P.sNx;
+  const int64_t yo1 = static_cast<int64_t>(ymap(1, my1)) * P.sNx;
+  const bool walls = __syncthreads_or(mx_lane || mx_last || my0 || my1);
+  constexpr int ROWS = 2 * F;
+  auto issue_raw = [&](int layer) {
+    const double* base = P.src + static_cast<int64_t>(layer) * P.s_layer;
+#pragma unroll 4
+    for (int r = warp; r < ROWS; r += NWARP) {
+      const double* rowp = base + static_cast<int64_t>(r >> 1) * P.s_plane + ((r & 1) ? yo1 : yo0);
+      cp_async8(raw + r * RAWX + lane, rowp + xo_lane);
+    }
+    if (tid < ROWS) {
+      const double* rowp = base + static_cast<int64_t>(tid >> 1) * P.s_plane + ((tid & 1) ? yo1 : yo0);
+      cp_async8(raw + tid * RAWX + TXC, rowp + xo_last);
+    }
+    cp_async_commit();
+  };
+  // mirror signs (zero-Dirichlet walls, PRE only): ghost = sigma (-1)^{a_n} interior
+  auto fix_walls = [&]() {
+    for (int e = tid; e < G::RAW; e += NTHREADS) {
+      const int r = e / RAWX, sx = e - r * RAWX;
+      const int f = r >> 1, sy = r & 1;
+      bool mx;
+      bool my;
+      (void)xmap(sx, mx);
+      (void)ymap(sy, my);
+      bool neg = false;
+      if (mx) neg ^= (((f / (n1 * n1)) & 1) != 0) ^ (P.comp != 0);
+      if (my) neg ^= ((((f / n1) % n1) & 1) != 0) ^ (P.comp != 1);
+      if (neg) raw[e] = -raw[e];
+    }
+  };
+  auto finish_raw = [&]() {
     cp_async_wait_all();
-    if (negmask) {
-#pragma unroll 1
-      for (int t = 0; t < G::RAW_PER_THREAD; ++t)
-        if ((negmask >> t) & 1u) raw[tid + t * NTHREADS] = -raw[tid + t * NTHREADS];
+    if (walls) {
+      __syncthreads();
+      fix_walls();
     }
     __syncthreads();
+  };
+  // targets: NT F rows of TXC cells, warp w streams rows w, w+8, ...
+  auto issue_targets = [&](int k) {
+    const int64_t lbase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + lane;
+    if (x0 + lane < P.tNx) {
+#pragma unroll 4
+      for (int r = warp; r < NT * F; r += NWARP) {
+        const int t = r / F, f = r - t * F;
+        cp_async8(tgs + r * TXC + lane, P.dst[t] + lbase + static_cast<int64_t>(f) * P.t_plane);
+      }
+    }
+    cp_async_commit();
   };
 
   // class of this warp in the Z + CK stage
@@ -212,7 +243,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
   const int cbase = ((PX * n + PY) * n1) * TXC + lane;
 
   // iteration k0-1 is the prologue: it only builds ring layer k0
-  issue_raw<MM>(raw, P.src + static_cast<int64_t>(k0) * P.s_layer, off, tid);
+  issue_raw(k0);
   double* ro = ring1;
   double* rn = ring0;
   bool bad = false;
@@ -220,22 +251,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
   for (int k = k0 - 1; k < k1; ++k) {
     const bool work = k >= k0;
     finish_raw();  // raw(k+1) landed; every warp left the previous Z + CK stage
-    if (work) {
-      // targets of layer k -> smem (async; consumed after the XY stage)
-      const int64_t lbase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0;
-#pragma unroll 1
-      for (int e = tid; e < NT * F * TXC; e += NTHREADS) {
-        const int cell = e & (TXC - 1);
-        const int tf = e >> 5;
-        const int t = tf / F, f = tf - t * F;
-        if (x0 + cell < P.tNx) cp_async8(tgs + e, P.dst[t] + lbase + f * P.t_plane + cell);
-      }
-      cp_async_commit();
-    }
+    if (work) issue_targets(k);  // consumed after the XY stage
     xy_task<MM>(P, warp, raw, rn, lane);
     cp_async_wait_all();
     __syncthreads();
-    if (k + 1 < k1) issue_raw<MM>(raw, P.src + static_cast<int64_t>(k + 2) * P.s_layer, off, tid);
+    if (k + 1 < k1) issue_raw(k + 2);
 
     if (work) {
       // Z stage + CK for this warp's parity class
@@ -354,6 +374,10 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
 bool tiled3d_supported(int m) { return m >= 1 && m <= 3; }
 
 int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st) {
+  // HLF_TILED_V5=1 selects the experimental 16-warp variant for m = 3 (A/B switch;
+  // it measured slower: shared-memory instruction queue bound)
+  static const bool use_v5 = std::getenv("HLF_TILED_V5") != nullptr;
+  if (m == 3 && use_v5) return v5::launch(kind, p, st);
   switch (m) {
     case 1: return launch_m<1>(kind, p, st);
     case 2: return launch_m<2>(kind, p, st);
