@@ -49,8 +49,13 @@ struct Cfg {
   static constexpr int RAW_PER_THREAD = (RAW + NTHREADS - 1) / NTHREADS;
   template <int NT>
   static constexpr int TGT = NT * F * TXC;
+  // NT == 1 (pressure), m < 3: raw and target stages are double-buffered so
+  // both loads get a whole layer iteration to land (+18 % at m = 1).  At m = 3
+  // it would fit (231 424 B) but leaves almost no L1 and measured 11 % slower.
   template <int NT>
-  static constexpr int SMEM_DOUBLES = RAW + 2 * RING + TGT<NT>;
+  static constexpr int NBUF = (NT == 1 && MM < 3) ? 2 : 1;
+  template <int NT>
+  static constexpr int SMEM_DOUBLES = NBUF<NT> * RAW + 2 * RING + NBUF<NT> * TGT<NT>;
 };
 
 struct TParams {
@@ -140,11 +145,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
   using G = Cfg<MM>;
   constexpr int n1 = G::n1, n = G::n, F = G::F, nh = G::nh, jh = G::jh;
   static_assert(nh == MM + 1, "n/2 == m+1");
+  constexpr int NB = G::template NBUF<NT>;
   extern __shared__ __align__(16) double smem[];
-  double* raw = smem;
-  double* ring0 = raw + G::RAW;
+  double* rawbuf = smem;                      // NB raw stages
+  double* ring0 = rawbuf + NB * G::RAW;
   double* ring1 = ring0 + G::RING;
-  double* tgs = ring1 + G::RING;  // targets of the current layer [t][f][cell]
+  double* tgsbuf = ring1 + G::RING;           // NB target stages [t][f][cell]
+  double* raw = rawbuf;
+  double* tgs = tgsbuf;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int x0 = blockIdx.x * TXC;
@@ -190,6 +198,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
   const bool walls = __syncthreads_or(mx_lane || mx_last || my0 || my1);
   constexpr int ROWS = 2 * F;
   auto issue_raw = [&](int layer) {
+    double* raw = rawbuf + (NB == 2 ? (layer & 1) : 0) * G::RAW;
     const double* base = P.src + static_cast<int64_t>(layer) * P.s_layer;
 #pragma unroll 4
     for (int r = warp; r < ROWS; r += NWARP) {
@@ -227,6 +236,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
   };
   // targets: NT F rows of TXC cells, warp w streams rows w, w+8, ...
   auto issue_targets = [&](int k) {
+    double* tgs = tgsbuf + (NB == 2 ? (k & 1) : 0) * (NT * F * TXC);
     const int64_t lbase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + lane;
     if (x0 + lane < P.tNx) {
 #pragma unroll 4
@@ -250,14 +260,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
 #pragma unroll 1
   for (int k = k0 - 1; k < k1; ++k) {
     const bool work = k >= k0;
-    finish_raw();  // raw(k+1) landed; every warp left the previous Z + CK stage
-    if (work) issue_targets(k);  // consumed after the XY stage
-    xy_task<MM>(P, warp, raw, rn, lane);
-    cp_async_wait_all();
-    __syncthreads();
-    if (k + 1 < k1) issue_raw(k + 2);
+    raw = rawbuf + (NB == 2 ? ((k + 1) & 1) : 0) * G::RAW;
+    tgs = tgsbuf + (NB == 2 ? (k & 1) : 0) * (NT * F * TXC);
+    if (NB == 2) {
+      // raw(k+1) and targets(k) landed; every warp left the previous Z + CK
+      // stage, so the other stages are free for raw(k+2) and targets(k+1)
+      finish_raw();
+      if (k + 1 < k1) issue_raw(k + 2);
+      if (k + 1 < k1 && k + 1 >= k0) issue_targets(k + 1);
+#ifndef HLF_EXP_NOXY
+      xy_task<MM>(P, warp, raw, rn, lane);
+#endif
+      __syncthreads();
+    } else {
+      finish_raw();  // raw(k+1) landed; every warp left the previous Z + CK stage
+#ifndef HLF_EXP_NOTGT
+      if (work) issue_targets(k);  // consumed after the XY stage
+#endif
+#ifndef HLF_EXP_NOXY
+      xy_task<MM>(P, warp, raw, rn, lane);
+#endif
+      cp_async_wait_all();
+      __syncthreads();
+      if (k + 1 < k1) issue_raw(k + 2);
+    }
 
+#ifdef HLF_EXP_NOZCK
+    if (0) {
+#else
     if (work) {
+#endif
       // Z stage + CK for this warp's parity class
       double pt[nh][nh][nh];
       z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
@@ -272,7 +304,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
           for (int b = 0; b < jh; ++b)
 #pragma unroll
             for (int d = 0; d < jh; ++d) acc[a][b][d] = 0.0;
+#ifndef HLF_EXP_NOCK
         ck<MM>(c, warp, P, pt, acc);
+#else
+        acc[0][0][0] += pt[0][0][0] + pt[3][3][3] + pt[1][2][3];
+#endif
         double* dstt = P.dst[t];
         const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
 #pragma unroll
