@@ -38,7 +38,7 @@ constexpr int TXC = 32;         // cells per CTA row (= lanes)
 constexpr int RAWX = TXC + 1;   // source nodes per row
 constexpr int NWARP = 8;
 constexpr int NTHREADS = NWARP * 32;
-constexpr int ZC = 32;          // target layers per CTA
+constexpr int ZC = 64;          // target layers per CTA
 constexpr int kMaxB = 20;       // multi-indices |b| <= 3
 
 template <int MM>
@@ -140,8 +140,11 @@ __device__ __forceinline__ void ck(int c, int w, const TParams& P, const double 
   else m3_ck(c, w, P, pt, acc);
 }
 
+// 1/o! for o <= 3 without a dynamically indexed parameter load
+__device__ __forceinline__ double ifact_s(int o) { return o <= 1 ? 1.0 : (o == 2 ? 0.5 : 1.0 / 6.0); }
+
 template <int MM, int NT>
-__global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ TParams P) {
+__global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid_constant__ TParams P) {
   using G = Cfg<MM>;
   constexpr int n1 = G::n1, n = G::n, F = G::F, nh = G::nh, jh = G::jh;
   static_assert(nh == MM + 1, "n/2 == m+1");
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tiled3d(const __grid_constant__ T
               const int oz = sz + 2 * d;
               if (ox > MM || oy > MM || oz > MM) continue;
               const int f = (ox * n1 + oy) * n1 + oz;
-              const double v = fma(acc[a][b][d], P.IF[ox] * P.IF[oy] * P.IF[oz], tgs[(t * F + f) * TXC + lane]);
+              const double v = fma(acc[a][b][d], ifact_s(ox) * ifact_s(oy) * ifact_s(oz), tgs[(t * F + f) * TXC + lane]);
               bad |= !isfinite(v);
               if (active) dstt[obase + f * P.t_plane] = v;
             }
