@@ -270,6 +270,8 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step) {
   int launched = -1;
   if (s->variant == 1 && !s->variable && s->d == 3 && hlfk::tiled3d_supported(s->m))
     launched = hlfk::launch_half_tiled3d(s->m, kind, P, s->stream);
+  else if (s->variant == 1 && !s->variable && s->d == 2 && hlfk::tiled2d_supported(s->m))
+    launched = hlfk::launch_half_tiled2d(s->m, kind, P, s->stream);
   if (launched == -2 || launched < 0 && s->variant != 1)  // -2: caller-supplied M differs from the baked one
     launched = hlfk::launch_half_generic(s->d, s->m, s->variable, kind, P, s->stream);
   if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
@@ -384,7 +386,8 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
   if (e != cudaSuccess) return bail(cuda_fail(s, e, "flag init"));
   e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) return bail(cuda_fail(s, e, "sync"));
-  s->variant = (d == 3 && !s->variable && hlfk::tiled3d_supported(s->m)) ? 1 : 0;
+  s->variant = !s->variable && ((d == 3 && hlfk::tiled3d_supported(s->m)) || (d == 2 && hlfk::tiled2d_supported(s->m)))
+                   ? 1 : 0;
   *out = s;
   return HLF_OK;
 }
@@ -635,8 +638,9 @@ int hlf_kernel_variant(const hlf_solver* s) { return s ? s->variant : -1; }
 
 hlf_status hlf_set_kernel_variant(hlf_solver* s, int variant) {
   if (!s) return HLF_INVALID_ARGUMENT;
-  if (variant == 1 && !(s->d == 3 && !s->variable && hlfk::tiled3d_supported(s->m)))
-    return fail(s, HLF_CONFIG_ERROR, "tiled 3D kernel not available for this configuration");
+  if (variant == 1 && !(!s->variable && ((s->d == 3 && hlfk::tiled3d_supported(s->m)) ||
+                                          (s->d == 2 && hlfk::tiled2d_supported(s->m)))))
+    return fail(s, HLF_CONFIG_ERROR, "tiled kernel not available for this configuration");
   if (variant != 0 && variant != 1) return fail(s, HLF_INVALID_ARGUMENT, "unknown variant");
   s->variant = variant;
   return HLF_OK;

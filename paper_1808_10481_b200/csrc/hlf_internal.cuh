@@ -61,6 +61,8 @@ int launch_half_generic(int d, int m, bool variable, HalfKind kind, const HalfPa
                         cudaStream_t st);
 int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
 bool tiled3d_supported(int m);
+int launch_half_tiled2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
+bool tiled2d_supported(int m);
 int launch_fill(const FillParams& p, cudaStream_t st);
 namespace v5 {
 // 16-warp tiled kernel, m = 3 (kernels_tiled3d_v5.cu)

@@ -1,0 +1,270 @@
+// Tiled, y-marching 2D half-step kernel (d = 2, constant coefficients, m = 1..4).
+//
+// One CTA = 4 warps owns a row of TXC = 32 target cells along x (lane = cell)
+// and marches over ZC target rows in y.  Per target row j:
+//   (raw)  the next source row (all (m+1)^2 coefficients of the 33 source
+//          nodes under the row) and the row's target jets stream into shared
+//          memory with cp.async one row ahead (double-buffered; ~40 KB per
+//          CTA, so several CTAs share an SM and keep HBM busy);
+//   (X)    half x-lines of M (reconstruct_cell_2d's first sweep,
+//          interpolation.cpp:87-99) into a 2-row ring;
+//   (Y+CK) warp = parity class (q_x, q_y mod 2): y half-lines between ring rows
+//          j and j+1 (interpolation.cpp:101-112), then the closed-form odd CK
+//          sum of the leapfrog update (d = 2) for every
+//          target component, added to the staged target and stored.
+// VEL (p -> v, u) is one launch; PRE (v, u -> p) is one launch per component.
+#include <cstring>
+
+#include "hlf_internal.cuh"
+
+namespace hlfk {
+namespace t2 {
+namespace {
+
+constexpr int TXC = 32;
+constexpr int RAWX = TXC + 1;
+constexpr int NWARP = 4;
+constexpr int NTHREADS = NWARP * 32;
+constexpr int ZC = 64;
+constexpr int kMaxB2 = 15;  // |b| <= 4 in 2D
+
+struct T2Params {
+  double ML[kMaxN * (kMaxM + 1)];  // s! M[s][l] (left block)
+  double GM[kMaxB2];               // G_k k!/b!
+  const double* src;
+  double* dst[2];
+  int64_t s_plane, t_plane;        // coefficient strides (Nx * Ny)
+  int sNx, sNy, tNx, tNy;
+  int K[2], bnd[2];
+  int pre, comp, step;
+  int* flag;
+};
+
+#include "tiled2d_gen.cuh"
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int MM>
+__device__ __forceinline__ void x_task(int px, const T2Params& P, const double* rb, double* wb) {
+  if constexpr (MM == 1) { if (px) t2_m1_x_px1(P, rb, wb); else t2_m1_x_px0(P, rb, wb); }
+  else if constexpr (MM == 2) { if (px) t2_m2_x_px1(P, rb, wb); else t2_m2_x_px0(P, rb, wb); }
+  else if constexpr (MM == 3) { if (px) t2_m3_x_px1(P, rb, wb); else t2_m3_x_px0(P, rb, wb); }
+  else { if (px) t2_m4_x_px1(P, rb, wb); else t2_m4_x_px0(P, rb, wb); }
+}
+
+template <int MM, int NT>
+__device__ __forceinline__ void yck(int w, const T2Params& P, const double* ro, const double* rn, const double* tg,
+                                    int lane, double* const* dptr, bool active, bool& bad) {
+#define HLF_T2(M_)                                                                     \
+  if (NT == 2) t2_m##M_##_vel(w, P, ro, rn, tg, lane, dptr, active, bad);              \
+  else if (P.comp == 0) t2_m##M_##_pre0(w, P, ro, rn, tg, lane, dptr, active, bad);    \
+  else t2_m##M_##_pre1(w, P, ro, rn, tg, lane, dptr, active, bad);
+  if constexpr (MM == 1) { HLF_T2(1) }
+  else if constexpr (MM == 2) { HLF_T2(2) }
+  else if constexpr (MM == 3) { HLF_T2(3) }
+  else { HLF_T2(4) }
+#undef HLF_T2
+}
+
+template <int MM, int NT>
+__global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Params P) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1;
+  constexpr int RAW = F * RAWX;
+  constexpr int RING = n * n1 * TXC;
+  constexpr int TGT = NT * F * TXC;
+  extern __shared__ __align__(16) double smem[];
+  double* rawbuf = smem;               // 2 stages
+  double* ring0 = rawbuf + 2 * RAW;
+  double* ring1 = ring0 + RING;
+  double* tgsbuf = ring1 + RING;       // 2 stages [t][f][cell]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int x0 = blockIdx.x * TXC;
+  const int j0 = blockIdx.y * ZC;
+  const int j1 = min(j0 + ZC, P.tNy);
+  if (j0 >= j1) return;
+  const bool active = x0 + lane < P.tNx;
+
+  // x node map of this lane and of node 32 (wrap, or mirror at walls)
+  auto xmap = [&](int sx, bool& mir) {
+    int q = x0 + sx - P.pre;
+    mir = false;
+    if (P.bnd[0] == 0) {
+      if (q >= P.K[0]) q -= P.K[0];
+      if (q < 0) q += P.K[0];
+    } else if (P.pre && (q < 0 || q == P.K[0])) {
+      q = q < 0 ? 0 : P.K[0] - 1;
+      mir = true;
+    }
+    return q >= P.sNx ? P.sNx - 1 : q;
+  };
+  auto ymap = [&](int r, bool& mir) {
+    int q = r;
+    mir = false;
+    if (P.bnd[1] == 0) {
+      if (q >= P.K[1]) q -= P.K[1];
+      if (q < 0) q += P.K[1];
+    } else if (P.pre && (q < 0 || q == P.K[1])) {
+      q = q < 0 ? 0 : P.K[1] - 1;
+      mir = true;
+    }
+    return q >= P.sNy ? P.sNy - 1 : q;
+  };
+  bool mx_lane, mx_last;
+  const int xo_lane = xmap(lane, mx_lane);
+  const int xo_last = xmap(TXC, mx_last);
+  const bool xwall = __syncthreads_or(mx_lane || mx_last);
+
+  // source row sr (allocation row index of the source family) -> raw stage
+  auto issue_raw = [&](int sr) {
+    double* raw = rawbuf + (sr & 1) * RAW;
+    bool my;
+    const int q = ymap(sr, my);
+    const double* rowbase = P.src + static_cast<int64_t>(q) * P.sNx;
+    for (int f = warp; f < F; f += NWARP) cp_async8(raw + f * RAWX + lane, rowbase + f * P.s_plane + xo_lane);
+    if (tid < F) cp_async8(raw + tid * RAWX + TXC, rowbase + tid * P.s_plane + xo_last);
+    cp_async_commit();
+  };
+  // mirror signs: ghost = sigma (-1)^{a_n} interior (zero-Dirichlet walls, PRE)
+  auto fix_raw = [&](int sr) {
+    bool my;
+    (void)ymap(sr, my);
+    if (!my && !xwall) return;
+    double* raw = rawbuf + (sr & 1) * RAW;
+    for (int e = tid; e < RAW; e += NTHREADS) {
+      const int f = e / RAWX, sx = e - f * RAWX;
+      bool mx;
+      (void)xmap(sx, mx);
+      bool neg = false;
+      if (mx) neg ^= ((f / n1) & 1) ^ (P.comp != 0);
+      if (my) neg ^= ((f % n1) & 1) ^ (P.comp != 1);
+      if (neg) raw[e] = -raw[e];
+    }
+  };
+  auto issue_targets = [&](int j) {
+    double* tg = tgsbuf + (j & 1) * TGT;
+    if (x0 + lane < P.tNx) {
+      const int64_t rowoff = static_cast<int64_t>(j) * P.tNx + x0 + lane;
+      for (int r = warp; r < NT * F; r += NWARP) {
+        const int t = r / F, f = r - t * F;
+        cp_async8(tg + r * TXC + lane, P.dst[t] + rowoff + f * P.t_plane);
+      }
+    }
+    cp_async_commit();
+  };
+
+  // source rows for target row j: j + s - pre, s = 0, 1
+  issue_raw(j0 - P.pre);
+  double* ro = ring1;
+  double* rn = ring0;
+  bool bad = false;
+  for (int j = j0 - 1; j < j1; ++j) {
+    const bool work = j >= j0;
+    const int snew = j + 1 - P.pre;  // source row entering the ring this iteration
+    cp_async_wait_all();
+    __syncthreads();
+    fix_raw(snew);
+    __syncthreads();
+    if (j + 1 < j1) issue_raw(snew + 1);
+    if (j + 1 < j1) issue_targets(j + 1);
+    const double* raw = rawbuf + (snew & 1) * RAW;
+    for (int task = warp; task < 2 * n1; task += NWARP) {
+      const int ly = task >> 1, px = task & 1;
+      x_task<MM>(px, P, raw + ly * RAWX + lane, rn + ly * TXC + lane);
+    }
+    __syncthreads();
+    if (work) {
+      double* dptr[NT];
+      for (int t = 0; t < NT; ++t) dptr[t] = P.dst[t] + static_cast<int64_t>(j) * P.tNx + x0 + lane;
+      yck<MM, NT>(warp, P, ro + lane, rn + lane, tgsbuf + (j & 1) * TGT, lane, dptr, active, bad);
+    }
+    double* tmp = ro;
+    ro = rn;
+    rn = tmp;
+  }
+  if (bad && active && P.step >= 0) atomicMin(P.flag, P.step);
+}
+
+double host_fact(int k) {
+  double r = 1.0;
+  for (int t = 2; t <= k; ++t) r *= t;
+  return r;
+}
+
+template <int MM, int NT>
+int launch_one(const T2Params& T, cudaStream_t st) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1;
+  const size_t smem = sizeof(double) * (2 * F * RAWX + 2 * n * n1 * TXC + 2 * NT * F * TXC);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tiled2d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+  dim3 grid((T.tNx + TXC - 1) / TXC, (T.tNy + ZC - 1) / ZC);
+  tiled2d<MM, NT><<<grid, NTHREADS, smem, st>>>(T);
+  return 1;
+}
+
+template <int MM>
+int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  T2Params T;
+  std::memset(&T, 0, sizeof(T));
+  for (int s = 0; s < n; ++s)
+    for (int l = 0; l < n1; ++l) T.ML[s * n1 + l] = host_fact(s) * p.M[s * n + l];
+  int idx = 0;
+  for (int b0 = 0; b0 <= MM; ++b0)
+    for (int b1 = 0; b1 <= MM - b0; ++b1) {
+      const int k = b0 + b1;
+      T.GM[idx++] = p.G[k] * host_fact(k) / (host_fact(b0) * host_fact(b1));
+    }
+  T.s_plane = p.s_coef;
+  T.t_plane = p.t_coef;
+  T.sNx = p.sNx;
+  T.sNy = p.sNy;
+  T.tNx = p.tNx;
+  T.tNy = p.tNy;
+  T.K[0] = p.K[0];
+  T.K[1] = p.K[1];
+  T.bnd[0] = p.bnd[0];
+  T.bnd[1] = p.bnd[1];
+  T.step = p.step;
+  T.flag = p.flag;
+  if (kind == VEL) {
+    T.src = p.src[0];
+    T.dst[0] = p.dst[0];
+    T.dst[1] = p.dst[1];
+    return launch_one<MM, 2>(T, st);
+  }
+  T.pre = 1;
+  int launched = 0;
+  for (int c = 0; c < 2; ++c) {
+    T.comp = c;
+    T.src = p.src[c];
+    T.dst[0] = p.dst[0];
+    launched += launch_one<MM, 1>(T, st);
+  }
+  return launched;
+}
+
+}  // namespace
+}  // namespace t2
+
+bool tiled2d_supported(int m) { return m >= 1 && m <= 4; }
+
+int launch_half_tiled2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st) {
+  switch (m) {
+    case 1: return t2::launch_m<1>(kind, p, st);
+    case 2: return t2::launch_m<2>(kind, p, st);
+    case 3: return t2::launch_m<3>(kind, p, st);
+    case 4: return t2::launch_m<4>(kind, p, st);
+    default: return -1;
+  }
+}
+
+}  // namespace hlfk

@@ -343,3 +343,13 @@ def test_z_slabs_on_one_gpu_match_single_domain(m):
         for r in range(2):
             got = slabs[r].get_field(f).reshape(K[0], K[1], kz, F)
             assert np.array_equal(got, ref[:, :, r * kz:(r + 1) * kz, :]), (f, r)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+@pytest.mark.parametrize("boundary", [[0, 0], [1, 1], [0, 1]])
+def test_parity_2d_tiled_kernel(m, boundary):
+    # crosses a partial 32-cell x tile and two 64-row y chunks
+    g, o = make_pair(2, m, [40, 70], boundary=boundary, seed=90 + m)
+    assert g.kernel_variant == 1
+    run_both(g, o, 5, 0.3 * g.grid.h)
+    compare(g, o, 2)
