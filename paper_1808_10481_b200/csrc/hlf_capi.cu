@@ -272,7 +272,7 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step) {
     launched = hlfk::launch_half_tiled3d(s->m, kind, P, s->stream);
   else if (s->variant == 1 && !s->variable && s->d == 2 && hlfk::tiled2d_supported(s->m))
     launched = hlfk::launch_half_tiled2d(s->m, kind, P, s->stream);
-  if (launched == -2 || launched < 0 && s->variant != 1)  // -2: caller-supplied M differs from the baked one
+  if (launched == -2 || launched < 0 && s->variant != 1)  // -2: custom M / planes too large for the tiled kernel
     launched = hlfk::launch_half_generic(s->d, s->m, s->variable, kind, P, s->stream);
   if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
   s->launches += launched;

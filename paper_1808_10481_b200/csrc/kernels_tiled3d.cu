@@ -66,6 +66,7 @@ struct TParams {
   double* dst[3];                  // target field bases, per target component
   int64_t s_layer, s_plane;        // source strides
   int64_t t_layer, t_plane;        // target strides
+  int t_plane32;                   // t_plane as int (host-checked: F * t_plane < 2^31)
   int sNx, sNy;                    // source plane dims (row stride = sNx)
   int tNx, tNy, tNz;               // target nodes
   int t_zoff;                      // target layer index of z = 0
@@ -102,6 +103,26 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 #include "tiled3d_gen.cuh"
+#include "tiled3d_v7_gen.cuh"
+// m = 3 Z + CK with both q_z parities in one warp (lanes 16..31 = PZ 1 of the
+// same 16 cells): the class-local CK body is picked by the warp-uniform
+// shift along x / y; along z the PZ = 0 lanes shift pt by one in registers.
+__device__ __forceinline__ void v7_ck(int c, int PX, int PY, int PZ, const TParams& P, double (&pt)[4][4][4],
+                                      double (&acc)[2][2][2]) {
+  if (c == 0) {
+    if (PX) v7_m3_ck_c0_s0(P, pt, acc); else v7_m3_ck_c0_s1(P, pt, acc);
+  } else if (c == 1) {
+    if (PY) v7_m3_ck_c1_s0(P, pt, acc); else v7_m3_ck_c1_s1(P, pt, acc);
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int d = 0; d < 4; ++d) pt[a][b][d] = PZ ? pt[a][b][d] : (d + 1 < 4 ? pt[a][b][d + 1] : 0.0);
+    v7_m3_ck_c2_s0(P, pt, acc);
+  }
+}
 
 template <int MM>
 __device__ __forceinline__ void xy_task(const TParams& P, int w, const double* raw, double* rn, int lane) {
@@ -163,7 +184,6 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   const int k0 = blockIdx.z * ZC;
   const int k1 = min(k0 + ZC, P.tNz);
   if (k0 >= k1) return;
-  const bool active = x0 + lane < P.tNx;
 
   // Raw layer = 2 F rows (f, source row sy) of RAWX nodes; warp w streams rows
   // w, w+8, ... with lane = node sx (sx = 32 of every row by thread tid < 2F).
@@ -252,8 +272,25 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   };
 
   // class of this warp in the Z + CK stage
-  const int PX = (warp >> 2) & 1, PY = (warp >> 1) & 1, PZ = warp & 1;
-  const int cbase = ((PX * n + PY) * n1) * TXC + lane;
+#ifndef HLF_NO_V7
+  constexpr bool V7 = MM == 3;
+#else
+  constexpr bool V7 = false;
+#endif
+  // V7 (m = 3): warp = (PX, PY, cell half), lane = (cell, PZ = lane >> 4)
+  const int PX = (warp >> 2) & 1, PY = (warp >> 1) & 1;
+  const int PZ = V7 ? (lane >> 4) : (warp & 1);
+  const int zcell = V7 ? ((warp & 1) * 16 + (lane & 15)) : lane;
+  const int cbase = ((PX * n + PY) * n1) * TXC + zcell;
+  const bool zactive = x0 + zcell < P.tNx;
+  double cz[nh][n1];
+  const double zg = PZ ? -1.0 : 1.0;
+  if constexpr (V7) {
+#pragma unroll
+    for (int iz = 0; iz < nh; ++iz)
+#pragma unroll
+      for (int l = 0; l < n1; ++l) cz[iz][l] = P.ML[(PZ + 2 * iz) * n1 + l];
+  }
 
   // iteration k0-1 is the prologue: it only builds ring layer k0
   issue_raw(k0);
@@ -295,8 +332,9 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
 #endif
       // Z stage + CK for this warp's parity class
       double pt[nh][nh][nh];
-      z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
-      const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + lane;
+      if constexpr (V7) v7_m3_z(ro + cbase, rn + cbase, cz, zg, pt);
+      else z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
+      const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
 #pragma unroll 1
       for (int t = 0; t < NT; ++t) {
         const int c = NT == 3 ? t : P.comp;
@@ -308,26 +346,31 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
 #pragma unroll
             for (int d = 0; d < jh; ++d) acc[a][b][d] = 0.0;
 #ifndef HLF_EXP_NOCK
-        ck<MM>(c, warp, P, pt, acc);
+        if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);
+        else ck<MM>(c, warp, P, pt, acc);
 #else
         acc[0][0][0] += pt[0][0][0] + pt[3][3][3] + pt[1][2][3];
 #endif
-        double* dstt = P.dst[t];
+        // outputs o = s + 2j (s = the class's output parity for component c):
+        // one base address per component, compile-time offsets per j
         const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
+        const int f0 = (sx * n1 + sy) * n1 + sz;
+        double* dp = P.dst[t] + obase + f0 * P.t_plane32;
+        const double* tp = tgs + (t * F + f0) * TXC + zcell;
+        const double ix[2] = {ifact_s(sx), ifact_s(sx + 2)};
+        const double iy[2] = {ifact_s(sy), ifact_s(sy + 2)};
+        const double iz[2] = {ifact_s(sz), ifact_s(sz + 2)};
 #pragma unroll
         for (int a = 0; a < jh; ++a) {
-          const int ox = sx + 2 * a;
 #pragma unroll
           for (int b = 0; b < jh; ++b) {
-            const int oy = sy + 2 * b;
 #pragma unroll
             for (int d = 0; d < jh; ++d) {
-              const int oz = sz + 2 * d;
-              if (ox > MM || oy > MM || oz > MM) continue;
-              const int f = (ox * n1 + oy) * n1 + oz;
-              const double v = fma(acc[a][b][d], ifact_s(ox) * ifact_s(oy) * ifact_s(oz), tgs[(t * F + f) * TXC + lane]);
+              if (MM < 3 && (sx + 2 * a > MM || sy + 2 * b > MM || sz + 2 * d > MM)) continue;
+              const int df = (2 * a * n1 + 2 * b) * n1 + 2 * d;
+              const double v = fma(acc[a][b][d], ix[a] * iy[b] * iz[d], tp[df * TXC]);
               bad |= !isfinite(v);
-              if (active) dstt[obase + f * P.t_plane] = v;
+              if (zactive) dp[df * P.t_plane32] = v;
             }
           }
         }
@@ -337,7 +380,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     ro = rn;
     rn = tmp;
   }
-  if (bad && active && P.step >= 0) atomicMin(P.flag, P.step);
+  if (bad && zactive && P.step >= 0) atomicMin(P.flag, P.step);
 }
 
 double host_fact(int k) {
@@ -378,6 +421,8 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.s_plane = p.s_coef;
   T.t_layer = p.t_layer;
   T.t_plane = p.t_coef;
+  if (static_cast<int64_t>(n1 * n1 * n1) * p.t_coef >= (int64_t{1} << 31)) return -2;  // generic path
+  T.t_plane32 = static_cast<int>(p.t_coef);
   T.sNx = p.sNx;
   T.sNy = p.sNy;
   T.tNx = p.tNx;

@@ -302,6 +302,74 @@ def main_v5():
     print("wrote", out)
 
 
+# ====================================================================== v7
+# Z + CK stage with the two q_z-parity classes in one warp (m = 3):
+#   warp = (PX, PY, cell half), lane = (cell in half, PZ = lane >> 4).
+# Both halves read the same ring words (shared-memory broadcast), the z half
+# line uses per-lane rows cz[iz][l] = s! M[PZ + 2 iz][l] and the per-lane sign
+# g = (-1)^PZ:  P~[PZ + 2 iz] = sum_l cz[iz][l] (L_l + g (-1)^l R_l).
+# The CK bodies are class-local (c, shift); the z shift of PZ = 0 lanes is an
+# in-register shift of pt before the z-component body.
+def v7_gen_z(mm):
+    n1, n = mm + 1, 2 * mm + 2
+    nh = n // 2
+    L = [f"__device__ __forceinline__ void v7_m{mm}_z(const double* __restrict__ ro, const double* __restrict__ rn,",
+         f"    const double (&cz)[{nh}][{n1}], double g, double (&pt)[{nh}][{nh}][{nh}]) {{",
+         "  // ro/rn = ring + ((PX*n + PY)*n1)*TXC + cell"]
+    for ix in range(nh):
+        for iy in range(nh):
+            off = ((2 * ix) * n + 2 * iy) * n1 * TXC
+            L.append("  {")
+            for l in range(n1):
+                sg = "g" if l % 2 == 0 else "-g"
+                L.append(f"    const double u{l} = fma({sg}, rn[{off + l * TXC}], ro[{off + l * TXC}]);")
+            for iz in range(nh):
+                expr = "0.0"
+                for l in range(n1):
+                    expr = f"fma(cz[{iz}][{l}], u{l}, {expr})"
+                L.append(f"    pt[{ix}][{iy}][{iz}] = {expr};")
+            L.append("  }")
+    L.append("}")
+    return "\n".join(L)
+
+
+def v7_gen_ck(mm, c, sh):
+    n1, n = mm + 1, 2 * mm + 2
+    nh, jh = n // 2, (n1 + 1) // 2
+    e = [int(c == a) for a in range(3)]
+    L = [f"__device__ __forceinline__ void v7_m{mm}_ck_c{c}_s{sh}(const TParams& P, const double (&pt)[{nh}][{nh}][{nh}],",
+         f"    double (&acc)[{jh}][{jh}][{jh}]) {{"]
+    for jx in range(jh):
+        for jy in range(jh):
+            for jz in range(jh):
+                j = (jx, jy, jz)
+                for b0 in range(mm + 1):
+                    for b1 in range(mm + 1 - b0):
+                        for b2 in range(mm + 1 - b0 - b1):
+                            b = (b0, b1, b2)
+                            i = [j[a] + b[a] + sh * e[a] for a in range(3)]
+                            if any(x >= nh for x in i):
+                                continue
+                            L.append(f"  acc[{jx}][{jy}][{jz}] = fma(P.GM[{bindex(b, mm)}], pt[{i[0]}][{i[1]}][{i[2]}], acc[{jx}][{jy}][{jz}]);")
+    L.append("}")
+    return "\n".join(L)
+
+
+def main_v7():
+    out = os.path.join(HERE, "..", "paper_1808_10481_b200", "csrc", "tiled3d_v7_gen.cuh")
+    mm = 3
+    parts = ["// GENERATED by tools/gen_tiled3d.py (v7) -- do not edit.",
+             "// Z + CK stage with q_z-parity pairs per warp, m = 3 (kernels_tiled3d.cu).", "#pragma once", "",
+             v7_gen_z(mm), ""]
+    for c in range(3):
+        for sh in range(2):
+            parts += [v7_gen_ck(mm, c, sh), ""]
+    with open(out, "w") as f:
+        f.write("\n".join(parts))
+    print("wrote", out)
+
+
 if __name__ == "__main__":
     main()
     main_v5()
+    main_v7()
