@@ -223,10 +223,21 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   auto issue_raw = [&](int layer) {
     double* raw = rawbuf + (NB == 2 ? (layer & 1) : 0) * G::RAW;
     const double* base = P.src + static_cast<int64_t>(layer) * P.s_layer;
+    if constexpr (ROWS % NWARP == 0) {
+      // row r = warp + 8 i: coefficient plane (warp >> 1) + 4 i, source row warp & 1
+      const double* q = base + static_cast<int64_t>(warp >> 1) * P.s_plane + ((warp & 1) ? yo1 : yo0) + xo_lane;
+      const int64_t step = (NWARP / 2) * P.s_plane;
+#pragma unroll
+      for (int i = 0; i < ROWS / NWARP; ++i) {
+        cp_async8(raw + (warp + NWARP * i) * RAWX + lane, q);
+        q += step;
+      }
+    } else {
 #pragma unroll 4
-    for (int r = warp; r < ROWS; r += NWARP) {
-      const double* rowp = base + static_cast<int64_t>(r >> 1) * P.s_plane + ((r & 1) ? yo1 : yo0);
-      cp_async8(raw + r * RAWX + lane, rowp + xo_lane);
+      for (int r = warp; r < ROWS; r += NWARP) {
+        const double* rowp = base + static_cast<int64_t>(r >> 1) * P.s_plane + ((r & 1) ? yo1 : yo0);
+        cp_async8(raw + r * RAWX + lane, rowp + xo_lane);
+      }
     }
     if (tid < ROWS) {
       const double* rowp = base + static_cast<int64_t>(tid >> 1) * P.s_plane + ((tid & 1) ? yo1 : yo0);
@@ -262,10 +273,24 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     double* tgs = tgsbuf + (NB == 2 ? (k & 1) : 0) * (NT * F * TXC);
     const int64_t lbase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + lane;
     if (x0 + lane < P.tNx) {
+      if constexpr (F % NWARP == 0) {
+        // row (t, f = warp + 8 i)
+        const int64_t step = NWARP * P.t_plane;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const double* q = P.dst[t] + lbase + static_cast<int64_t>(warp) * P.t_plane;
+#pragma unroll
+          for (int i = 0; i < F / NWARP; ++i) {
+            cp_async8(tgs + (t * F + warp + NWARP * i) * TXC + lane, q);
+            q += step;
+          }
+        }
+      } else {
 #pragma unroll 4
-      for (int r = warp; r < NT * F; r += NWARP) {
-        const int t = r / F, f = r - t * F;
-        cp_async8(tgs + r * TXC + lane, P.dst[t] + lbase + static_cast<int64_t>(f) * P.t_plane);
+        for (int r = warp; r < NT * F; r += NWARP) {
+          const int t = r / F, f = r - t * F;
+          cp_async8(tgs + r * TXC + lane, P.dst[t] + lbase + static_cast<int64_t>(f) * P.t_plane);
+        }
       }
     }
     cp_async_commit();
