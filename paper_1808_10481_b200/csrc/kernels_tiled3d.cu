@@ -49,13 +49,15 @@ struct Cfg {
   static constexpr int RAW_PER_THREAD = (RAW + NTHREADS - 1) / NTHREADS;
   template <int NT>
   static constexpr int TGT = NT * F * TXC;
-  // NT == 1 (pressure), m < 3: raw and target stages are double-buffered so
-  // both loads get a whole layer iteration to land (+18 % at m = 1).  At m = 3
-  // it would fit (231 424 B) but leaves almost no L1 and measured 11 % slower.
+  // NT == 1 (pressure), m < 3: the raw stage is double-buffered so the source
+  // layer gets a whole iteration to land (+18 % at m = 1).  At m = 3 the 8-warp
+  // CTA has no shared memory left for it.  Targets are single-buffered: every
+  // staged target value is read by exactly one lane, which reloads its slots
+  // for the next layer right after its epilogue (no barrier needed).
   template <int NT>
   static constexpr int NBUF = (NT == 1 && MM < 3) ? 2 : 1;
   template <int NT>
-  static constexpr int SMEM_DOUBLES = NBUF<NT> * RAW + 2 * RING + NBUF<NT> * TGT<NT>;
+  static constexpr int SMEM_DOUBLES = NBUF<NT> * RAW + 2 * RING + TGT<NT>;
 };
 
 struct TParams {
@@ -99,8 +101,17 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void st_global(double* p, double v) {
+  asm volatile("st.global.f64 [%0], %1;\n" ::"l"(__cvta_generic_to_global(p)), "d"(v));
+}
+// cp.async that the compiler may not reorder with the surrounding shared-memory
+// reads (the target slots are re-filled right after their last read)
+__device__ __forceinline__ void cp_async8_ordered(double* smem, const double* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 #include "tiled3d_gen.cuh"
 #include "tiled3d_v7_gen.cuh"
@@ -174,9 +185,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   double* rawbuf = smem;                      // NB raw stages
   double* ring0 = rawbuf + NB * G::RAW;
   double* ring1 = ring0 + G::RING;
-  double* tgsbuf = ring1 + G::RING;           // NB target stages [t][f][cell]
+  double* tgs = ring1 + G::RING;              // target stage [t][f][cell], lane-private entries
   double* raw = rawbuf;
-  double* tgs = tgsbuf;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int x0 = blockIdx.x * TXC;
@@ -261,41 +271,13 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     }
   };
   auto finish_raw = [&]() {
-    cp_async_wait_all();
+    cp_async_wait_group1();  // this thread's raw(k+1) landed; its targets(k) may be in flight
     if (walls) {
       __syncthreads();
       fix_walls();
     }
     __syncthreads();
   };
-  // targets: NT F rows of TXC cells, warp w streams rows w, w+8, ...
-  auto issue_targets = [&](int k) {
-    double* tgs = tgsbuf + (NB == 2 ? (k & 1) : 0) * (NT * F * TXC);
-    const int64_t lbase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + lane;
-    if (x0 + lane < P.tNx) {
-      if constexpr (F % NWARP == 0) {
-        // row (t, f = warp + 8 i)
-        const int64_t step = NWARP * P.t_plane;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const double* q = P.dst[t] + lbase + static_cast<int64_t>(warp) * P.t_plane;
-#pragma unroll
-          for (int i = 0; i < F / NWARP; ++i) {
-            cp_async8(tgs + (t * F + warp + NWARP * i) * TXC + lane, q);
-            q += step;
-          }
-        }
-      } else {
-#pragma unroll 4
-        for (int r = warp; r < NT * F; r += NWARP) {
-          const int t = r / F, f = r - t * F;
-          cp_async8(tgs + r * TXC + lane, P.dst[t] + lbase + static_cast<int64_t>(f) * P.t_plane);
-        }
-      }
-    }
-    cp_async_commit();
-  };
-
   // class of this warp in the Z + CK stage
 #ifndef HLF_NO_V7
   constexpr bool V7 = MM == 3;
@@ -317,37 +299,55 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       for (int l = 0; l < n1; ++l) cz[iz][l] = P.ML[(PZ + 2 * iz) * n1 + l];
   }
 
+  // Targets of layer kk for this lane's own outputs (the entries its epilogue
+  // reads), staged with cp.async one iteration ahead.  Per-thread cp.async
+  // groups: every iteration commits [raw(k+2)] then [targets(k+1)], so
+  // wait_group 1 at the top (raw) and before the epilogue (targets) suffices.
+  auto issue_own_targets = [&](int kk) {
+    if (zactive) {
+      const int64_t ob = static_cast<int64_t>(P.t_zoff + kk) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
+#pragma unroll 1
+      for (int t = 0; t < NT; ++t) {
+        const int c = NT == 3 ? t : P.comp;
+        const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
+        const int f0 = (sx * n1 + sy) * n1 + sz;
+        const double* q = P.dst[t] + ob + f0 * P.t_plane32;
+        double* sp = tgs + (t * F + f0) * TXC + zcell;
+#pragma unroll
+        for (int a = 0; a < jh; ++a)
+#pragma unroll
+          for (int b = 0; b < jh; ++b)
+#pragma unroll
+            for (int d = 0; d < jh; ++d) {
+              if (MM < 3 && (sx + 2 * a > MM || sy + 2 * b > MM || sz + 2 * d > MM)) continue;
+              const int df = (2 * a * n1 + 2 * b) * n1 + 2 * d;
+              cp_async8_ordered(sp + df * TXC, q + df * P.t_plane32);
+            }
+      }
+    }
+    cp_async_commit();
+  };
+
   // iteration k0-1 is the prologue: it only builds ring layer k0
   issue_raw(k0);
+  cp_async_commit();  // (empty) targets group of the prologue
   double* ro = ring1;
   double* rn = ring0;
-  bool bad = false;
+  int emax = 0;  // max |high word| of the written values (finite check)
 #pragma unroll 1
   for (int k = k0 - 1; k < k1; ++k) {
     const bool work = k >= k0;
     raw = rawbuf + (NB == 2 ? ((k + 1) & 1) : 0) * G::RAW;
-    tgs = tgsbuf + (NB == 2 ? (k & 1) : 0) * (NT * F * TXC);
+    finish_raw();  // raw(k+1) landed; every warp left the previous Z + CK stage
     if (NB == 2) {
-      // raw(k+1) and targets(k) landed; every warp left the previous Z + CK
-      // stage, so the other stages are free for raw(k+2) and targets(k+1)
-      finish_raw();
-      if (k + 1 < k1) issue_raw(k + 2);
-      if (k + 1 < k1 && k + 1 >= k0) issue_targets(k + 1);
+      if (k + 1 < k1) issue_raw(k + 2); else cp_async_commit();
+    }
 #ifndef HLF_EXP_NOXY
-      xy_task<MM>(P, warp, raw, rn, lane);
+    xy_task<MM>(P, warp, raw, rn, lane);
 #endif
-      __syncthreads();
-    } else {
-      finish_raw();  // raw(k+1) landed; every warp left the previous Z + CK stage
-#ifndef HLF_EXP_NOTGT
-      if (work) issue_targets(k);  // consumed after the XY stage
-#endif
-#ifndef HLF_EXP_NOXY
-      xy_task<MM>(P, warp, raw, rn, lane);
-#endif
-      cp_async_wait_all();
-      __syncthreads();
-      if (k + 1 < k1) issue_raw(k + 2);
+    __syncthreads();
+    if (NB == 1) {
+      if (k + 1 < k1) issue_raw(k + 2); else cp_async_commit();
     }
 
 #ifdef HLF_EXP_NOZCK
@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       if constexpr (V7) v7_m3_z(ro + cbase, rn + cbase, cz, zg, pt);
       else z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
       const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
+      cp_async_wait_group1();  // this lane's targets(k) landed; raw(k+2) may be in flight
 #pragma unroll 1
       for (int t = 0; t < NT; ++t) {
         const int c = NT == 3 ? t : P.comp;
@@ -370,18 +371,19 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
           for (int b = 0; b < jh; ++b)
 #pragma unroll
             for (int d = 0; d < jh; ++d) acc[a][b][d] = 0.0;
+        // outputs o = s + 2j (s = the class's output parity for component c):
+        // one base address per component, compile-time offsets per j
+        const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
+        const int f0 = (sx * n1 + sy) * n1 + sz;
+        double* dp = P.dst[t] + obase + f0 * P.t_plane32;
+        asm("" : "+l"(dp));  // keep dp a base register: one IMAD.WIDE per output address
+        const double* tp = tgs + (t * F + f0) * TXC + zcell;
 #ifndef HLF_EXP_NOCK
         if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);
         else ck<MM>(c, warp, P, pt, acc);
 #else
         acc[0][0][0] += pt[0][0][0] + pt[3][3][3] + pt[1][2][3];
 #endif
-        // outputs o = s + 2j (s = the class's output parity for component c):
-        // one base address per component, compile-time offsets per j
-        const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
-        const int f0 = (sx * n1 + sy) * n1 + sz;
-        double* dp = P.dst[t] + obase + f0 * P.t_plane32;
-        const double* tp = tgs + (t * F + f0) * TXC + zcell;
         const double ix[2] = {ifact_s(sx), ifact_s(sx + 2)};
         const double iy[2] = {ifact_s(sy), ifact_s(sy + 2)};
         const double iz[2] = {ifact_s(sz), ifact_s(sz + 2)};
@@ -394,18 +396,23 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
               if (MM < 3 && (sx + 2 * a > MM || sy + 2 * b > MM || sz + 2 * d > MM)) continue;
               const int df = (2 * a * n1 + 2 * b) * n1 + 2 * d;
               const double v = fma(acc[a][b][d], ix[a] * iy[b] * iz[d], tp[df * TXC]);
-              bad |= !isfinite(v);
-              if (zactive) dp[df * P.t_plane32] = v;
+              emax = max(emax, __double2hiint(v) & 0x7fffffff);  // >= 0x7ff00000: inf / nan
+              if (zactive) st_global(dp + df * P.t_plane32, v);
             }
           }
         }
       }
     }
+#ifndef HLF_EXP_NOTGT
+    if (k + 1 < k1) issue_own_targets(k + 1); else cp_async_commit();
+#else
+    cp_async_commit();
+#endif
     double* tmp = ro;
     ro = rn;
     rn = tmp;
   }
-  if (bad && zactive && P.step >= 0) atomicMin(P.flag, P.step);
+  if (emax >= 0x7ff00000 && zactive && P.step >= 0) atomicMin(P.flag, P.step);
 }
 
 double host_fact(int k) {

@@ -21,10 +21,18 @@ for c in range(1, d + 1):
     g.fill_separable(c, -0.1, [pi] * d, [pi / 2 if a == c - 1 else 0.0 for a in range(d)])
 dt = 0.9 * g.grid.h / math.sqrt(d)
 g.set_times(0, dt / 2, dt)
-g.advance_n(2)
+# HLF_EXP_* ablation builds produce garbage: time them without the finite check
+check = os.environ.get("HLF_NOCHECK") is None
+def run(k):
+    try:
+        g.advance_n(k)
+    except H.InstabilityError:
+        if check:
+            raise
+run(2)
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record(stream)
-g.advance_n(steps)
+run(steps)
 e1.record(stream)
 e1.synchronize()
 ms = e0.elapsed_time(e1) / steps
