@@ -110,7 +110,7 @@ def cpu_reference_arm(args, steps, warmup):
     3D stepper, so this is the oracle port (oracle/hlf_oracle.cpp,
     the d-dim restatement that is bit-identical to the compiled reference in 1D),
     run with every host thread on a bounded sample of the same 3D m=3 periodic
-    mode.  Returns (DOF-updates/s, sample description, threads)."""
+    mode.  Returns (DOF-updates/s, sample description, threads, ms per sample step)."""
     import numpy as np
     import oracle as O
     threads = os.cpu_count() or 1
@@ -130,7 +130,8 @@ def cpu_reference_arm(args, steps, warmup):
     o.advance_n(steps)
     sec = time.perf_counter() - t0
     dof = 4 * F * K ** 3
-    return dof * steps / sec, f"oracle port, 3D m=3 periodic {K}^3 cells, {steps} steps after {warmup} warm-up", threads
+    return (dof * steps / sec, f"oracle port, 3D m=3 periodic {K}^3 cells, {steps} steps after {warmup} warm-up",
+            threads, sec / steps * 1e3)
 
 
 def run_reference_impl(args):
@@ -138,10 +139,11 @@ def run_reference_impl(args):
     if rank != 0:
         return
     steps, warmup = args.steps, args.warmup
-    value, sample, threads = cpu_reference_arm(args, steps, warmup)
+    value, sample, threads, sample_ms = cpu_reference_arm(args, steps, warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": warmup, "ms_per_step": None, "higher_is_better": True,
+        # one step = one leapfrog step of the bounded 24^3 sample (the metric is a rate)
+        "steps": steps, "warmup": warmup, "ms_per_step": sample_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "3D acoustic Hermite-leapfrog m=3 periodic (CPU sample of the 512x512x256-per-GPU job)",
                    "m": M},
@@ -251,7 +253,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sample, threads = cpu_reference_arm(args, 2, 1)
+        v, sample, threads, _ = cpu_reference_arm(args, 2, 1)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
 
     if rank == 0:
