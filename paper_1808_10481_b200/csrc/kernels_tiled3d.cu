@@ -47,8 +47,14 @@ struct Cfg {
   static constexpr int RAW = F * 2 * RAWX;
   static constexpr int RING = n * n * n1 * TXC;
   static constexpr int RAW_PER_THREAD = (RAW + NTHREADS - 1) / NTHREADS;
+  // NT: 3 = velocity half (three targets), 1 = one pressure divergence term,
+  // 2 = merged V_x + V_y pressure launch (two raw sources, one target; m = 3)
   template <int NT>
-  static constexpr int TGT = NT * F * TXC;
+  static constexpr int NTGT = NT == 2 ? 1 : NT;
+  template <int NT>
+  static constexpr int NRAW = NT == 2 ? 2 : ((NT == 1 && MM < 3) ? 2 : 1);
+  template <int NT>
+  static constexpr int TGT = NTGT<NT> * F * TXC;
   // NT == 1 (pressure), m < 3: the raw stage is double-buffered so the source
   // layer gets a whole iteration to land (+18 % at m = 1).  At m = 3 the 8-warp
   // CTA has no shared memory left for it.  Targets are single-buffered: every
@@ -57,7 +63,7 @@ struct Cfg {
   template <int NT>
   static constexpr int NBUF = (NT == 1 && MM < 3) ? 2 : 1;
   template <int NT>
-  static constexpr int SMEM_DOUBLES = NBUF<NT> * RAW + 2 * RING + TGT<NT>;
+  static constexpr int SMEM_DOUBLES = NRAW<NT> * RAW + 2 * RING + TGT<NT>;
 };
 
 struct TParams {
@@ -65,6 +71,7 @@ struct TParams {
   double GM[kMaxB];                // G_k * k!/b!, indexed by bindex(b)
   double IF[kMaxM + 1];            // 1/o!
   const double* src;               // source field base (layer 0 of the allocation)
+  const double* src2;              // NT == 2: the V_y source
   double* dst[3];                  // target field bases, per target component
   int64_t s_layer, s_plane;        // source strides
   int64_t t_layer, t_plane;        // target strides
@@ -120,7 +127,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 // shift along x / y; along z the PZ = 0 lanes shift pt by one in registers.
 __device__ __forceinline__ void v7_ck(int c, int PX, int PY, int PZ, const TParams& P, double (&pt)[4][4][4],
                                       double (&acc)[2][2][2]) {
-  if (c == 0) {
+  if (c < 0) {
+    v7_m3_ck_c0_s0(P, pt, acc);  // no shift (merged pressure launch)
+  } else if (c == 0) {
     if (PX) v7_m3_ck_c0_s0(P, pt, acc); else v7_m3_ck_c0_s1(P, pt, acc);
   } else if (c == 1) {
     if (PY) v7_m3_ck_c1_s0(P, pt, acc); else v7_m3_ck_c1_s1(P, pt, acc);
@@ -181,9 +190,12 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   constexpr int n1 = G::n1, n = G::n, F = G::F, nh = G::nh, jh = G::jh;
   static_assert(nh == MM + 1, "n/2 == m+1");
   constexpr int NB = G::template NBUF<NT>;
+  constexpr bool MX = NT == 2;                // merged V_x + V_y pressure launch
+  constexpr int NTT = G::template NTGT<NT>;   // target fields
+  static_assert(!MX || MM == 3, "merged pressure launch is generated for m = 3");
   extern __shared__ __align__(16) double smem[];
-  double* rawbuf = smem;                      // NB raw stages
-  double* ring0 = rawbuf + NB * G::RAW;
+  double* rawbuf = smem;                      // NB raw stages (MX: raw V_x, raw V_y)
+  double* ring0 = rawbuf + G::template NRAW<NT> * G::RAW;
   double* ring1 = ring0 + G::RING;
   double* tgs = ring1 + G::RING;              // target stage [t][f][cell], lane-private entries
   double* raw = rawbuf;
@@ -231,8 +243,10 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   const bool walls = __syncthreads_or(mx_lane || mx_last || my0 || my1);
   constexpr int ROWS = 2 * F;
   auto issue_raw = [&](int layer) {
-    double* raw = rawbuf + (NB == 2 ? (layer & 1) : 0) * G::RAW;
-    const double* base = P.src + static_cast<int64_t>(layer) * P.s_layer;
+#pragma unroll
+   for (int si = 0; si < (MX ? 2 : 1); ++si) {
+    double* raw = rawbuf + (MX ? si : (NB == 2 ? (layer & 1) : 0)) * G::RAW;
+    const double* base = (si ? P.src2 : P.src) + static_cast<int64_t>(layer) * P.s_layer;
     if constexpr (ROWS % NWARP == 0) {
       // row r = warp + 8 i: coefficient plane (warp >> 1) + 4 i, source row warp & 1
       const double* q = base + static_cast<int64_t>(warp >> 1) * P.s_plane + ((warp & 1) ? yo1 : yo0) + xo_lane;
@@ -253,10 +267,11 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       const double* rowp = base + static_cast<int64_t>(tid >> 1) * P.s_plane + ((tid & 1) ? yo1 : yo0);
       cp_async8(raw + tid * RAWX + TXC, rowp + xo_last);
     }
+   }
     cp_async_commit();
   };
   // mirror signs (zero-Dirichlet walls, PRE only): ghost = sigma (-1)^{a_n} interior
-  auto fix_walls = [&]() {
+  auto fix_walls_buf = [&](double* raw, int comp) {
     for (int e = tid; e < G::RAW; e += NTHREADS) {
       const int r = e / RAWX, sx = e - r * RAWX;
       const int f = r >> 1, sy = r & 1;
@@ -265,9 +280,17 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       (void)xmap(sx, mx);
       (void)ymap(sy, my);
       bool neg = false;
-      if (mx) neg ^= (((f / (n1 * n1)) & 1) != 0) ^ (P.comp != 0);
-      if (my) neg ^= ((((f / n1) % n1) & 1) != 0) ^ (P.comp != 1);
+      if (mx) neg ^= (((f / (n1 * n1)) & 1) != 0) ^ (comp != 0);
+      if (my) neg ^= ((((f / n1) % n1) & 1) != 0) ^ (comp != 1);
       if (neg) raw[e] = -raw[e];
+    }
+  };
+  auto fix_walls = [&]() {
+    if constexpr (MX) {
+      fix_walls_buf(rawbuf, 0);
+      fix_walls_buf(rawbuf + G::RAW, 1);
+    } else {
+      fix_walls_buf(raw, P.comp);
     }
   };
   auto finish_raw = [&]() {
@@ -307,8 +330,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     if (zactive) {
       const int64_t ob = static_cast<int64_t>(P.t_zoff + kk) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
 #pragma unroll 1
-      for (int t = 0; t < NT; ++t) {
-        const int c = NT == 3 ? t : P.comp;
+      for (int t = 0; t < NTT; ++t) {
+        const int c = MX ? -1 : (NT == 3 ? t : P.comp);
         const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
         const int f0 = (sx * n1 + sy) * n1 + sz;
         const double* q = P.dst[t] + ob + f0 * P.t_plane32;
@@ -343,7 +366,21 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       if (k + 1 < k1) issue_raw(k + 2); else cp_async_commit();
     }
 #ifndef HLF_EXP_NOXY
-    xy_task<MM>(P, warp, raw, rn, lane);
+    if constexpr (MX) {
+      const int lz = warp >> 1;
+      double* wb = rn + lz * TXC + lane;
+      const double* rbx = rawbuf + lz * 2 * RAWX + lane;
+      const double* rby = rbx + G::RAW;
+      if (warp & 1) {
+        m3_xy_px1_vx(P, rbx, wb);
+        m3_xy_px1_vy(P, rby, wb);
+      } else {
+        m3_xy_px0_vx(P, rbx, wb);
+        m3_xy_px0_vy(P, rby, wb);
+      }
+    } else {
+      xy_task<MM>(P, warp, raw, rn, lane);
+    }
 #endif
     __syncthreads();
     if (NB == 1) {
@@ -362,8 +399,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
       cp_async_wait_group1();  // this lane's targets(k) landed; raw(k+2) may be in flight
 #pragma unroll 1
-      for (int t = 0; t < NT; ++t) {
-        const int c = NT == 3 ? t : P.comp;
+      for (int t = 0; t < NTT; ++t) {
+        const int c = MX ? -1 : (NT == 3 ? t : P.comp);  // -1: shifts already in the XY rows
         double acc[jh][jh][jh];
 #pragma unroll
         for (int a = 0; a < jh; ++a)
@@ -475,11 +512,24 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
     return launch_one<MM, 3>(T, st);
   }
   T.pre = 1;
+  T.dst[0] = p.dst[0];
   int launched = 0;
+  static const bool merge = std::getenv("HLF_NO_MERGE") == nullptr;
+  if constexpr (MM == 3) {
+    if (merge) {
+      // V_x and V_y divergence terms in one launch, V_z in a second
+      T.comp = -1;
+      T.src = p.src[0];
+      T.src2 = p.src[1];
+      launched += launch_one<MM, 2>(T, st);
+      T.comp = 2;
+      T.src = p.src[2];
+      return launched + launch_one<MM, 1>(T, st);
+    }
+  }
   for (int c = 0; c < 3; ++c) {
     T.comp = c;
     T.src = p.src[c];
-    T.dst[0] = p.dst[0];
     launched += launch_one<MM, 1>(T, st);
   }
   return launched;

@@ -41,34 +41,45 @@ def bindex(b, mm):
     raise ValueError(b)
 
 
-def half_line(mm, srcL, srcR, outs, tmp, lines):
-    """outputs s in `outs` of a parity-split line from L/R expressions."""
-    n1 = mm + 1
+def half_line(mm, srcL, srcR, outs, tmp, lines, sh=0):
+    """outputs s in `outs` of a parity-split line from L/R expressions.  sh = 1
+    uses row s+1 of M for output s (the index shift of a divergence term,
+    merged pressure kernel); rows past 2m+1 give the literal 0.0."""
+    n1, n = mm + 1, 2 * mm + 2
     need_s, need_d = set(), set()
     for s in outs:
+        if s + sh >= n:
+            continue
         for l in range(n1):
-            (need_s if (s + l) % 2 == 0 else need_d).add(l)
+            (need_s if (s + sh + l) % 2 == 0 else need_d).add(l)
     for l in sorted(need_s):
         lines.append(f"  const double {tmp}s{l} = {srcL(l)} + {srcR(l)};")
     for l in sorted(need_d):
         lines.append(f"  const double {tmp}d{l} = {srcR(l)} - {srcL(l)};")
     res = {}
     for s in outs:
+        r = s + sh
+        if r >= n:
+            res[s] = "0.0"
+            continue
         expr = "0.0"
         for l in range(n1):
-            if (s + l) % 2 == 0:
-                expr = f"fma(P.ML[{s * n1 + l}], {tmp}s{l}, {expr})"
+            if (r + l) % 2 == 0:
+                expr = f"fma(P.ML[{r * n1 + l}], {tmp}s{l}, {expr})"
             else:
-                expr = f"fma(-P.ML[{s * n1 + l}], {tmp}d{l}, {expr})"
+                expr = f"fma(-P.ML[{r * n1 + l}], {tmp}d{l}, {expr})"
         name = f"{tmp}o{s}"
         lines.append(f"  const double {name} = {expr};")
         res[s] = name
     return res
 
 
-def gen_xy(mm, px):
+def gen_xy(mm, px, shx=0, shy=0, acc=False, suffix=""):
+    """fused X+Y task; shx / shy shift the x / y rows (merged pressure kernel:
+    V_x enters through rows q_x+1, V_y through rows q_y+1); acc adds into the
+    ring instead of storing."""
     n1, n = mm + 1, 2 * mm + 2
-    L = [f"__device__ __forceinline__ void m{mm}_xy_px{px}(const TParams& P, const double* __restrict__ rb,",
+    L = [f"__device__ __forceinline__ void m{mm}_xy_px{px}{suffix}(const TParams& P, const double* __restrict__ rb,",
          "                                                  double* __restrict__ wb) {",
          "  // rb = raw + l_z*2*RAWX + lane;  wb = ring_new + l_z*TXC + lane"]
     qxs = [q for q in range(n) if q % 2 == px]
@@ -77,14 +88,24 @@ def gen_xy(mm, px):
         for ly in range(n1):
             def off(lx, side, sy=sy, ly=ly):
                 return f"rb[{((lx * n1 * n1 + ly * n1) * 2 + sy) * RAWX + side}]"
-            res = half_line(mm, lambda l: off(l, 0), lambda l: off(l, 1), qxs, f"x{sy}{ly}", L)
+            res = half_line(mm, lambda l: off(l, 0), lambda l: off(l, 1), qxs, f"x{sy}{ly}", L, shx)
             for q, nm in res.items():
                 xh[(sy, ly, q)] = nm
     for qx in qxs:
+        if qx + shx >= n:  # the whole x row is zero
+            if not acc:
+                for qy in range(n):
+                    L.append(f"  wb[{(qx * n + qy) * n1 * TXC}] = 0.0;")
+            continue
         res = half_line(mm, lambda l, qx=qx: xh[(0, l, qx)], lambda l, qx=qx: xh[(1, l, qx)],
-                        list(range(n)), f"y{qx}", L)
+                        list(range(n)), f"y{qx}", L, shy)
         for qy, nm in res.items():
-            L.append(f"  wb[{(qx * n + qy) * n1 * TXC}] = {nm};")
+            o = (qx * n + qy) * n1 * TXC
+            if acc:
+                if nm != "0.0":
+                    L.append(f"  wb[{o}] += {nm};")
+            else:
+                L.append(f"  wb[{o}] = {nm};")
     L.append("}")
     return "\n".join(L)
 
@@ -153,6 +174,12 @@ def main():
         for px in range(2):
             parts.append(gen_xy(mm, px))
             parts.append("")
+            if mm == 3:
+                # merged pressure (V_x + V_y) launch: C = (My x Mx^{+1}) V_x + (My^{+1} x Mx) V_y
+                parts.append(gen_xy(mm, px, shx=1, suffix="_vx"))
+                parts.append("")
+                parts.append(gen_xy(mm, px, shy=1, acc=True, suffix="_vy"))
+                parts.append("")
         for pz in range(2):
             parts.append(gen_z(mm, pz))
             parts.append("")
