@@ -371,6 +371,9 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       double* wb = rn + lz * TXC + lane;
       const double* rbx = rawbuf + lz * 2 * RAWX + lane;
       const double* rby = rbx + G::RAW;
+#ifndef HLF_XY_RMW
+      if (warp & 1) m3_xy_px1_vxy(P, rbx, rby, wb); else m3_xy_px0_vxy(P, rbx, rby, wb);
+#else
       if (warp & 1) {
         m3_xy_px1_vx(P, rbx, wb);
         m3_xy_px1_vy(P, rby, wb);
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
         m3_xy_px0_vx(P, rbx, wb);
         m3_xy_px0_vy(P, rby, wb);
       }
+#endif
     } else {
       xy_task<MM>(P, warp, raw, rn, lane);
     }

@@ -110,6 +110,41 @@ def gen_xy(mm, px, shx=0, shy=0, acc=False, suffix=""):
     return "\n".join(L)
 
 
+def gen_xy_merged(mm, px):
+    """merged pressure XY task: C = (My x Mx^{+1}) V_x + (My^{+1} x Mx) V_y for
+    the task's q_x parity, summed in registers (one ring store per value)."""
+    n1, n = mm + 1, 2 * mm + 2
+    L = [f"__device__ __forceinline__ void m{mm}_xy_px{px}_vxy(const TParams& P, const double* __restrict__ rbx,",
+         "    const double* __restrict__ rby, double* __restrict__ wb) {",
+         "  // rbx / rby = raw V_x / raw V_y + l_z*2*RAWX + lane;  wb = ring_new + l_z*TXC + lane"]
+    qxs = [q for q in range(n) if q % 2 == px]
+    xh = {}
+    for fld, rb, shx in (("a", "rbx", 1), ("b", "rby", 0)):
+        for sy in range(2):
+            for ly in range(n1):
+                def off(lx, side, sy=sy, ly=ly, rb=rb):
+                    return f"{rb}[{((lx * n1 * n1 + ly * n1) * 2 + sy) * RAWX + side}]"
+                res = half_line(mm, lambda l: off(l, 0), lambda l: off(l, 1), qxs, f"{fld}{sy}{ly}", L, shx)
+                for q, nm in res.items():
+                    xh[(fld, sy, ly, q)] = nm
+    for qx in qxs:
+        parts = {}
+        for fld, shy in (("a", 0), ("b", 1)):
+            if fld == "a" and qx + 1 >= n:
+                continue  # V_x row q_x+1 does not exist
+            res = half_line(mm, lambda l, qx=qx, fld=fld: xh[(fld, 0, l, qx)],
+                            lambda l, qx=qx, fld=fld: xh[(fld, 1, l, qx)], list(range(n)), f"y{fld}{qx}", L, shy)
+            for qy, nm in res.items():
+                if nm != "0.0":
+                    parts.setdefault(qy, []).append(nm)
+        for qy in range(n):
+            terms = parts.get(qy, [])
+            expr = " + ".join(terms) if terms else "0.0"
+            L.append(f"  wb[{(qx * n + qy) * n1 * TXC}] = {expr};")
+    L.append("}")
+    return "\n".join(L)
+
+
 def gen_z(mm, pz):
     n1, n = mm + 1, 2 * mm + 2
     nh = n // 2
@@ -179,6 +214,8 @@ def main():
                 parts.append(gen_xy(mm, px, shx=1, suffix="_vx"))
                 parts.append("")
                 parts.append(gen_xy(mm, px, shy=1, acc=True, suffix="_vy"))
+                parts.append("")
+                parts.append(gen_xy_merged(mm, px))
                 parts.append("")
         for pz in range(2):
             parts.append(gen_z(mm, pz))
