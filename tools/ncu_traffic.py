@@ -13,7 +13,10 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ALG = {"tiled3d<3, 1>": 1536, "tiled3d<3, 3>": 3584}  # algorithmic bytes per cell
+# algorithmic bytes per cell and launch: V_z pressure launch
+# reads 1 source + p read/write; merged V_x+V_y reads 2 sources + p; velocity
+# reads p + 3 v read/write
+ALG = {"tiled3d<3, 1>": 1536, "tiled3d<3, 2>": 2048, "tiled3d<3, 3>": 3584}
 
 
 def main(path, nz):
@@ -38,6 +41,7 @@ def main(path, nz):
                          "duration_unit": units[hdr.index("gpu__time_duration.sum")],
                          "duration": float(r[hdr.index("gpu__time_duration.sum")])})
     pre = [l["bytes_per_cell"] for l in launches if "<3, 1>" in l["kernel"]]
+    vel = [l["bytes_per_cell"] for l in launches if "<3, 3>" in l["kernel"]]
     res = {"source": f"ncu --set full of `bench.py --steps 1 --warmup 3 --nz {nz}` (the bench workload with {nz} "
                      "instead of 256 z layers per GPU; identical CTA/tile/z-chunk structure); per-cell bytes "
                      "scaled to 512x512x256",
@@ -45,6 +49,9 @@ def main(path, nz):
     if pre:
         res["pre_bytes_per_cell"] = sum(pre) / len(pre)
         res["pre_dram_bytes_per_launch"] = res["pre_bytes_per_cell"] * 512 * 512 * 256
+    if vel:
+        res["vel_bytes_per_cell"] = sum(vel) / len(vel)
+        res["vel_dram_bytes_per_launch"] = res["vel_bytes_per_cell"] * 512 * 512 * 256
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1))
