@@ -12,7 +12,12 @@
 //          j and j+1 (interpolation.cpp:101-112), then the closed-form odd CK
 //          sum of the leapfrog update (d = 2) for every
 //          target component, added to the staged target and stored.
-// VEL (p -> v, u) is one launch; PRE (v, u -> p) is one launch per component.
+// VEL (p -> v, u) is one launch (NT = 2).  PRE (v, u -> p) at m <= 3 is one
+// merged launch (NT = 3): P~ = My (Mx^{+1} V_x) + My^{+1} (Mx V_y), i.e. the
+// index shift of each divergence term moves into that term's sweep rows, so
+// both terms share one CK sum and one read-modify-write of p; at m = 4 it is
+// one launch per component (NT = 1).
+#include <cstdlib>
 #include <cstring>
 
 #include "hlf_internal.cuh"
@@ -32,6 +37,7 @@ struct T2Params {
   double ML[kMaxN * (kMaxM + 1)];  // s! M[s][l] (left block)
   double GM[kMaxB2];               // G_k k!/b!
   const double* src;
+  const double* src2;              // NT == 3: the V_y source
   double* dst[2];
   int64_t s_plane, t_plane;        // coefficient strides (Nx * Ny)
   int sNx, sNy, tNx, tNy;
@@ -57,6 +63,24 @@ __device__ __forceinline__ void x_task(int px, const T2Params& P, const double* 
   else { if (px) t2_m4_x_px1(P, rb, wb); else t2_m4_x_px0(P, rb, wb); }
 }
 
+template <int MM>
+__device__ __forceinline__ void x_task_sh(int px, const T2Params& P, const double* rb, double* wb) {
+  if constexpr (MM == 1) { if (px) t2_m1_x_px1_sh(P, rb, wb); else t2_m1_x_px0_sh(P, rb, wb); }
+  else if constexpr (MM == 2) { if (px) t2_m2_x_px1_sh(P, rb, wb); else t2_m2_x_px0_sh(P, rb, wb); }
+  else if constexpr (MM == 3) { if (px) t2_m3_x_px1_sh(P, rb, wb); else t2_m3_x_px0_sh(P, rb, wb); }
+  else { if (px) t2_m4_x_px1_sh(P, rb, wb); else t2_m4_x_px0_sh(P, rb, wb); }
+}
+
+template <int MM>
+__device__ __forceinline__ void yck_merged(int w, const T2Params& P, const double* ro, const double* rn,
+                                           const double* rob, const double* rnb, const double* tg, int lane,
+                                           double* const* dptr, bool active, bool& bad) {
+  if constexpr (MM == 1) t2_m1_prem(w, P, ro, rn, rob, rnb, tg, lane, dptr, active, bad);
+  else if constexpr (MM == 2) t2_m2_prem(w, P, ro, rn, rob, rnb, tg, lane, dptr, active, bad);
+  else if constexpr (MM == 3) t2_m3_prem(w, P, ro, rn, rob, rnb, tg, lane, dptr, active, bad);
+  else t2_m4_prem(w, P, ro, rn, rob, rnb, tg, lane, dptr, active, bad);
+}
+
 template <int MM, int NT>
 __device__ __forceinline__ void yck(int w, const T2Params& P, const double* ro, const double* rn, const double* tg,
                                     int lane, double* const* dptr, bool active, bool& bad) {
@@ -74,14 +98,19 @@ __device__ __forceinline__ void yck(int w, const T2Params& P, const double* ro, 
 template <int MM, int NT>
 __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Params P) {
   constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1;
+  constexpr bool MX = NT == 3;         // merged pressure launch
+  constexpr int NS = MX ? 2 : 1;       // raw sources
+  constexpr int NTT = MX ? 1 : NT;     // target fields
   constexpr int RAW = F * RAWX;
   constexpr int RING = n * n1 * TXC;
-  constexpr int TGT = NT * F * TXC;
+  constexpr int TGT = NTT * F * TXC;
   extern __shared__ __align__(16) double smem[];
-  double* rawbuf = smem;               // 2 stages
-  double* ring0 = rawbuf + 2 * RAW;
+  double* rawbuf = smem;               // [source][2 stages]
+  double* ring0 = rawbuf + 2 * NS * RAW;
   double* ring1 = ring0 + RING;
-  double* tgsbuf = ring1 + RING;       // 2 stages [t][f][cell]
+  double* ringb0 = ring1 + RING;       // MX: x-lines of V_y (ring A = ring0/1 holds V_x's)
+  double* ringb1 = ringb0 + (MX ? RING : 0);
+  double* tgsbuf = ringb1 + (MX ? RING : 0);  // 2 stages [t][f][cell]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int x0 = blockIdx.x * TXC;
@@ -122,12 +151,15 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
 
   // source row sr (allocation row index of the source family) -> raw stage
   auto issue_raw = [&](int sr) {
-    double* raw = rawbuf + (sr & 1) * RAW;
     bool my;
     const int q = ymap(sr, my);
-    const double* rowbase = P.src + static_cast<int64_t>(q) * P.sNx;
-    for (int f = warp; f < F; f += NWARP) cp_async8(raw + f * RAWX + lane, rowbase + f * P.s_plane + xo_lane);
-    if (tid < F) cp_async8(raw + tid * RAWX + TXC, rowbase + tid * P.s_plane + xo_last);
+#pragma unroll
+    for (int si = 0; si < NS; ++si) {
+      double* raw = rawbuf + (si * 2 + (sr & 1)) * RAW;
+      const double* rowbase = (si ? P.src2 : P.src) + static_cast<int64_t>(q) * P.sNx;
+      for (int f = warp; f < F; f += NWARP) cp_async8(raw + f * RAWX + lane, rowbase + f * P.s_plane + xo_lane);
+      if (tid < F) cp_async8(raw + tid * RAWX + TXC, rowbase + tid * P.s_plane + xo_last);
+    }
     cp_async_commit();
   };
   // mirror signs: ghost = sigma (-1)^{a_n} interior (zero-Dirichlet walls, PRE)
@@ -135,22 +167,25 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
     bool my;
     (void)ymap(sr, my);
     if (!my && !xwall) return;
-    double* raw = rawbuf + (sr & 1) * RAW;
-    for (int e = tid; e < RAW; e += NTHREADS) {
-      const int f = e / RAWX, sx = e - f * RAWX;
-      bool mx;
-      (void)xmap(sx, mx);
-      bool neg = false;
-      if (mx) neg ^= ((f / n1) & 1) ^ (P.comp != 0);
-      if (my) neg ^= ((f % n1) & 1) ^ (P.comp != 1);
-      if (neg) raw[e] = -raw[e];
+    for (int si = 0; si < NS; ++si) {
+      double* raw = rawbuf + (si * 2 + (sr & 1)) * RAW;
+      const int comp = MX ? si : P.comp;
+      for (int e = tid; e < RAW; e += NTHREADS) {
+        const int f = e / RAWX, sx = e - f * RAWX;
+        bool mx;
+        (void)xmap(sx, mx);
+        bool neg = false;
+        if (mx) neg ^= ((f / n1) & 1) ^ (comp != 0);
+        if (my) neg ^= ((f % n1) & 1) ^ (comp != 1);
+        if (neg) raw[e] = -raw[e];
+      }
     }
   };
   auto issue_targets = [&](int j) {
     double* tg = tgsbuf + (j & 1) * TGT;
     if (x0 + lane < P.tNx) {
       const int64_t rowoff = static_cast<int64_t>(j) * P.tNx + x0 + lane;
-      for (int r = warp; r < NT * F; r += NWARP) {
+      for (int r = warp; r < NTT * F; r += NWARP) {
         const int t = r / F, f = r - t * F;
         cp_async8(tg + r * TXC + lane, P.dst[t] + rowoff + f * P.t_plane);
       }
@@ -162,6 +197,8 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
   issue_raw(j0 - P.pre);
   double* ro = ring1;
   double* rn = ring0;
+  double* rob = ringb1;
+  double* rnb = ringb0;
   bool bad = false;
   for (int j = j0 - 1; j < j1; ++j) {
     const bool work = j >= j0;
@@ -173,19 +210,35 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
     if (j + 1 < j1) issue_raw(snew + 1);
     if (j + 1 < j1) issue_targets(j + 1);
     const double* raw = rawbuf + (snew & 1) * RAW;
-    for (int task = warp; task < 2 * n1; task += NWARP) {
-      const int ly = task >> 1, px = task & 1;
-      x_task<MM>(px, P, raw + ly * RAWX + lane, rn + ly * TXC + lane);
+    if constexpr (MX) {
+      // V_x with the shifted x rows into ring A, V_y into ring B
+      for (int task = warp; task < 4 * n1; task += NWARP) {
+        const int si = task >= 2 * n1, tk = task - si * 2 * n1, ly = tk >> 1, px = tk & 1;
+        if (si) x_task<MM>(px, P, raw + 2 * RAW + ly * RAWX + lane, rnb + ly * TXC + lane);
+        else x_task_sh<MM>(px, P, raw + ly * RAWX + lane, rn + ly * TXC + lane);
+      }
+    } else {
+      for (int task = warp; task < 2 * n1; task += NWARP) {
+        const int ly = task >> 1, px = task & 1;
+        x_task<MM>(px, P, raw + ly * RAWX + lane, rn + ly * TXC + lane);
+      }
     }
     __syncthreads();
     if (work) {
-      double* dptr[NT];
-      for (int t = 0; t < NT; ++t) dptr[t] = P.dst[t] + static_cast<int64_t>(j) * P.tNx + x0 + lane;
-      yck<MM, NT>(warp, P, ro + lane, rn + lane, tgsbuf + (j & 1) * TGT, lane, dptr, active, bad);
+      double* dptr[NTT];
+      for (int t = 0; t < NTT; ++t) dptr[t] = P.dst[t] + static_cast<int64_t>(j) * P.tNx + x0 + lane;
+      if constexpr (MX)
+        yck_merged<MM>(warp, P, ro + lane, rn + lane, rob + lane, rnb + lane, tgsbuf + (j & 1) * TGT, lane, dptr,
+                       active, bad);
+      else
+        yck<MM, NT>(warp, P, ro + lane, rn + lane, tgsbuf + (j & 1) * TGT, lane, dptr, active, bad);
     }
     double* tmp = ro;
     ro = rn;
     rn = tmp;
+    tmp = rob;
+    rob = rnb;
+    rnb = tmp;
   }
   if (bad && active && P.step >= 0) atomicMin(P.flag, P.step);
 }
@@ -199,7 +252,8 @@ double host_fact(int k) {
 template <int MM, int NT>
 int launch_one(const T2Params& T, cudaStream_t st) {
   constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1;
-  const size_t smem = sizeof(double) * (2 * F * RAWX + 2 * n * n1 * TXC + 2 * NT * F * TXC);
+  constexpr int NS = NT == 3 ? 2 : 1, NTT = NT == 3 ? 1 : NT;
+  const size_t smem = sizeof(double) * (2 * NS * F * RAWX + 2 * NS * n * n1 * TXC + 2 * NTT * F * TXC);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tiled2d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -242,6 +296,19 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
     return launch_one<MM, 2>(T, st);
   }
   T.pre = 1;
+  // merged launch, 4096^2 step times: m = 1 +13 %, m = 2 +9 %, m = 3 +9 %;
+  // at m = 4 its larger shared footprint (two raw sources, four ring rows)
+  // costs occupancy and it is 14 % slower, so there the per-component
+  // launches stay (HLF_MERGE_ALL forces the merged launch for A/B runs)
+  static const bool merge = std::getenv("HLF_NO_MERGE") == nullptr;
+  static const bool merge_all = std::getenv("HLF_MERGE_ALL") != nullptr;
+  if (merge && (MM <= 3 || merge_all)) {
+    T.comp = -1;
+    T.src = p.src[0];
+    T.src2 = p.src[1];
+    T.dst[0] = p.dst[0];
+    return launch_one<MM, 3>(T, st);
+  }
   int launched = 0;
   for (int c = 0; c < 2; ++c) {
     T.comp = c;
