@@ -1,0 +1,78 @@
+"""Device throughput of every SURVEY.md sec. 8(d) configuration through the
+public Python API (CUDA events on the solver stream, warm-up steps first).
+The headline 3D line is bench.py's; this script records the others:
+
+  cfg1   1D m=3 standing wave, K=256 (143 steps) and K=2^24
+  cfg2   2D periodic acoustics mode, K=1024, m=1..4 (+ 4096^2 m=3)
+  cfg3   2D walls, K=4096, m=3, variable c^2 jets (generic iterated kernel)
+  cfg4   3D periodic, 512x512x256, m=1..3 (bench.py's workload)
+
+Usage: python tools/bench_configs.py [out.json]"""
+import json
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1808_10481_b200 as H
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HBM = 6551.4e9  # MEASURED_PEAKS.json hbm_gbs
+
+
+def timed(g, stream, steps, warm=3):
+    g.advance_n(warm)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    g.advance_n(steps, warm)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run(name, d, m, K, boundary=None, variable=False, steps=20):
+    stream = torch.cuda.Stream()
+    Ks = list(K)
+    g = H.Stepper(H.Grid([-1.0] * d, 2.0 / Ks[0], tuple(Ks)), m, boundary=boundary, variable_ap=variable,
+                  stream=stream.cuda_stream)
+    pi = math.pi
+    g.fill_separable(0, 1.0, [pi] * d, [0.0] * d)
+    if variable:
+        for grid in (0, 1):
+            jets = np.zeros((g.num_nodes(grid), g.E))
+            jets[:, 0] = -1.0  # ap = -c^2 with c^2 = 1 (the iterated variable-coefficient path)
+            g.set_coeff(grid, jets)
+    dt = 0.9 * g.grid.h / math.sqrt(d)
+    g.set_times(0.0, dt / 2, dt)
+    ms = timed(g, stream, steps)
+    dof = (d + 1) * (m + 1) ** d * math.prod(Ks)
+    rate = dof / (ms * 1e-3)
+    line = {"config": name, "d": d, "m": m, "K": Ks, "boundary": boundary or [0] * d, "variable_c2": variable,
+            "kernel": "tiled" if g.kernel_variant == 1 else "generic", "ms_per_step": ms,
+            "dof_updates_per_s": rate, "hbm_frac_24B": 24 * rate / HBM}
+    print(json.dumps(line), flush=True)
+    del g
+    torch.cuda.empty_cache()
+    return line
+
+
+def main():
+    out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r1", "configs.json")
+    res = [run("cfg1", 1, 3, [256], steps=143), run("cfg1 large", 1, 3, [1 << 24], steps=20)]
+    for m in (1, 2, 3, 4):
+        res.append(run("cfg2", 2, m, [1024, 1024], steps=100))
+    res.append(run("cfg2 large", 2, 3, [4096, 4096], steps=20))
+    res.append(run("cfg3", 2, 3, [4096, 4096], boundary=[1, 1], variable=True, steps=3))
+    for m in (1, 2, 3):
+        res.append(run("cfg4", 3, m, [512, 512, 256], steps=5))
+    with open(out, "w") as f:
+        json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
