@@ -2,7 +2,8 @@
 // (d<=2: m<=8; d=3: m<=4).  One thread per target node; the stacked corner
 // tensor and the reconstruction live in thread-local arrays.  This is the
 // correctness path for every configuration and the production path for 1D;
-// the 3D headline runs the tiled kernel in kernels_tiled3d.cu.
+// the 3D headline runs the tiled kernel in kernels_tiled3d.cu.  In 1D the
+// same arithmetic runs fully unrolled in registers (half_1d).
 //
 // Per target node:
 //   1. gather the (m+1)^d jets of the 2^d source corners into the stacked
@@ -254,12 +255,131 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
   if (bad && P.step >= 0) atomicMin(P.flag, P.step);
 }
 
+// 1D: the same faithful arithmetic, operation for operation (so results stay
+// bit-identical to half_generic<1,...>, the oracle and the compiled
+// reference), but fully unrolled: every array index is a compile-time
+// constant, the 2n stacked values, the two n-entry tables and the target jet
+// live in registers, and the kernel streams at memory speed instead of
+// spilling its tables to local memory.
+template <int MM, bool VAR, int KIND>
+__global__ void __launch_bounds__(128) half_1d(const __grid_constant__ HalfParams P) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  const int t0 = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t0 >= P.tNx) return;
+  // corner nodes (same maps as half_generic)
+  int q[2];
+  bool flip[2];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    int qq = KIND == VEL ? t0 + side : t0 - 1 + side;
+    flip[side] = false;
+    if (P.bnd[0] == 0) {
+      if (qq >= P.K[0]) qq -= P.K[0];
+      if (qq < 0) qq += P.K[0];
+    } else if (KIND == PRE) {
+      if (qq < 0) {
+        qq = 0;
+        flip[side] = true;
+      } else if (qq >= P.K[0]) {
+        qq = P.K[0] - 1;
+        flip[side] = true;
+      }
+    }
+    q[side] = qq;
+  }
+  double S[n];
+#pragma unroll
+  for (int side = 0; side < 2; ++side)
+#pragma unroll
+    for (int a = 0; a < n1; ++a) {
+      const double v = __ldg(P.src[0] + q[side] + a * P.s_coef);
+      S[side * n1 + a] = (flip[side] && (a & 1)) ? -v : v;  // ghost = (-1)^a interior (normal velocity)
+    }
+  double T[n];  // M applied along x (interpolation.cpp:53-61)
+#pragma unroll
+  for (int r = 0; r < n; ++r) {
+    double acc = 0.0;
+#pragma unroll
+    for (int s2 = 0; s2 < n; ++s2) acc = __dadd_rn(acc, __dmul_rn(P.M[r * n + s2], S[s2]));
+    T[r] = acc;
+  }
+  double Pt[n], Vt[n];
+#pragma unroll
+  for (int e = 0; e < n; ++e) {
+    Pt[e] = KIND == VEL ? T[e] : 0.0;
+    Vt[e] = KIND == VEL ? 0.0 : T[e];
+  }
+  const int64_t toff = t0;
+  double tgt[n1];
+#pragma unroll
+  for (int f = 0; f < n1; ++f) tgt[f] = P.dst[0][toff + f * P.t_coef];
+  const double* apj = VAR ? P.coeff + t0 : nullptr;
+  // CK recurrence, count = 2m+2 levels (stepper1d.cpp:22-38)
+#pragma unroll
+  for (int r = 0; r + 1 < n; ++r) {
+    const bool p_live = (KIND == VEL) == (r % 2 == 0);
+    if (p_live) {
+#pragma unroll
+      for (int e = 0; e < n; ++e) {
+        const double dv = e + 1 < n ? __ddiv_rn(__dmul_rn(Pt[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P.h)
+                                    : 0.0;
+        Vt[e] = __dmul_rn(P.av, dv);
+      }
+    } else {
+      double Sd[n];
+#pragma unroll
+      for (int e = 0; e < n; ++e) {
+        const double dv = e + 1 < n ? __ddiv_rn(__dmul_rn(Vt[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P.h)
+                                    : 0.0;
+        Sd[e] = __dadd_rn(0.0, dv);
+      }
+      if (VAR) {
+#pragma unroll
+        for (int e = 0; e < n; ++e) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int ei = 0; ei <= e; ++ei) {
+            const double a = __ldg(apj + ei * P.c_coef);
+            if (a != 0.0) sacc = __dadd_rn(sacc, __dmul_rn(a, Sd[e - ei]));
+          }
+          Pt[e] = sacc;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < n; ++e) Pt[e] = __dmul_rn(P.ap, Sd[e]);
+      }
+    }
+    if ((r + 1) & 1) {  // leapfrog_half_update (stepper1d.cpp:54-61)
+      const double w = P.w[r + 1];
+#pragma unroll
+      for (int f = 0; f < n1; ++f) tgt[f] = __dadd_rn(tgt[f], __dmul_rn(w, KIND == VEL ? Vt[f] : Pt[f]));
+    }
+  }
+  bool bad = false;
+#pragma unroll
+  for (int f = 0; f < n1; ++f) {
+    bad |= !isfinite(tgt[f]);
+    P.dst[0][toff + f * P.t_coef] = tgt[f];
+  }
+  if (bad && P.step >= 0) atomicMin(P.flag, P.step);
+}
+
 template <int D, int MM>
 int launch_dm(bool variable, HalfKind kind, const HalfParams& p, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(p.tNx) * p.tNy * p.tNz;
   const int threads = 128;
   const unsigned blocks = static_cast<unsigned>((total + threads - 1) / threads);
   if (blocks == 0) return 0;
+  if constexpr (D == 1) {
+    if (kind == VEL) {
+      if (variable) half_1d<MM, true, VEL><<<blocks, threads, 0, st>>>(p);
+      else half_1d<MM, false, VEL><<<blocks, threads, 0, st>>>(p);
+    } else {
+      if (variable) half_1d<MM, true, PRE><<<blocks, threads, 0, st>>>(p);
+      else half_1d<MM, false, PRE><<<blocks, threads, 0, st>>>(p);
+    }
+    return 1;
+  }
   if (kind == VEL) {
     if (variable) half_generic<D, MM, true, VEL><<<blocks, threads, 0, st>>>(p);
     else half_generic<D, MM, false, VEL><<<blocks, threads, 0, st>>>(p);
