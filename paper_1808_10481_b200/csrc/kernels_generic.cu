@@ -168,6 +168,11 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
   const double* apj = VAR ? P.coeff + static_cast<int64_t>(D == 3 ? t[2] : 0) * P.c_layer +
                                 static_cast<int64_t>(D >= 2 ? t[1] : 0) * P.tNx + t[0]
                           : nullptr;
+  double apl[VAR ? E : 1];  // this node's ap jet, loaded once for all CK levels
+  if constexpr (VAR) {
+#pragma unroll 1
+    for (int e = 0; e < E; ++e) apl[e] = __ldg(apj + e * P.c_coef);
+  }
 #pragma unroll 1
   for (int r = 0; r + 1 < n; ++r) {
     const bool p_live = (KIND == VEL) == (r % 2 == 0);
@@ -198,27 +203,32 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
       }
       if (VAR) {
         // truncated tensor product, contributions in ascending order of the
-        // ap index (jet.cpp:109-121)
+        // ap index (jet.cpp:109-121): for output q only ap indices qi <= q
+        // (per axis) contribute, visited as nested ascending loops, which is
+        // the ascending flat order of the reference's full scan
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
           int q[3] = {0, 0, 0};
           Idx<D>::template split<n>(e, q);
           double s = 0.0;
+          if constexpr (D == 2) {
 #pragma unroll 1
-          for (int ei = 0; ei < E; ++ei) {
-            int qi[3] = {0, 0, 0};
-            Idx<D>::template split<n>(ei, qi);
-            bool ok = true;
-            int qr[3] = {0, 0, 0};
-#pragma unroll
-            for (int ax = 0; ax < D; ++ax) {
-              qr[ax] = q[ax] - qi[ax];
-              if (qr[ax] < 0) ok = false;
-            }
-            if (!ok) continue;
-            const double a = __ldg(apj + ei * P.c_coef);
-            if (a == 0.0) continue;
-            s = __dadd_rn(s, __dmul_rn(a, S[Idx<D>::template flat<n>(qr)]));
+            for (int ix = 0; ix <= q[0]; ++ix)
+#pragma unroll 1
+              for (int iy = 0; iy <= q[1]; ++iy) {
+                const double a = apl[ix * n + iy];
+                if (a != 0.0) s = __dadd_rn(s, __dmul_rn(a, S[(q[0] - ix) * n + (q[1] - iy)]));
+              }
+          } else {
+#pragma unroll 1
+            for (int ix = 0; ix <= q[0]; ++ix)
+#pragma unroll 1
+              for (int iy = 0; iy <= q[1]; ++iy)
+#pragma unroll 1
+                for (int iz = 0; iz <= q[2]; ++iz) {
+                  const double a = apl[(ix * n + iy) * n + iz];
+                  if (a != 0.0) s = __dadd_rn(s, __dmul_rn(a, S[((q[0] - ix) * n + (q[1] - iy)) * n + (q[2] - iz)]));
+                }
           }
           Pt[e] = s;
         }
