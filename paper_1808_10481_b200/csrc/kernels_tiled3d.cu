@@ -237,6 +237,10 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   const bool walls = __syncthreads_or(mx_lane || mx_last || my0 || my1);
   constexpr int ROWS = 2 * F;
   auto issue_raw = [&](int layer) {
+#ifdef HLF_EXP_NORAW
+    cp_async_commit();
+    return;
+#endif
 #pragma unroll
    for (int si = 0; si < (MX ? 2 : 1); ++si) {
     double* raw = rawbuf + (MX ? si : (NB == 2 ? (layer & 1) : 0)) * G::RAW;
