@@ -103,6 +103,15 @@ hlf_status hlf_advance_v(hlf_solver* s);
    for callers that interleave halo exchanges (z slabs) */
 hlf_status hlf_advance_p_indexed(hlf_solver* s, int step_index);
 hlf_status hlf_advance_v_indexed(hlf_solver* s, int step_index);
+/* One half step over target layers [z_begin, z_end) only (3D; half 0 =
+   pressure, 1 = velocity), without advancing the time stamp: a z-slab rank
+   updates its interior layers while the halo layer is in flight and the
+   boundary layer after it lands, then calls hlf_commit_half once.  Same
+   arithmetic as the full launch (advance_p/advance_v, stepper1d.cpp:147-166,
+   restricted to a layer range). */
+hlf_status hlf_advance_layers(hlf_solver* s, int half, int step_index, int z_begin, int z_end);
+/* t_p (half 0) or t_v (half 1) += dt, as advance_p/advance_v do (stepper1d.cpp:155,165) */
+hlf_status hlf_commit_half(hlf_solver* s, int half);
 /* advance_p, advance_v, finite check: HLF_INSTABILITY (synchronous) if the
    state became non-finite; message "solution became non-finite at step N" */
 hlf_status hlf_step(hlf_solver* s, int step_index);

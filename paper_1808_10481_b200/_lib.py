@@ -21,7 +21,8 @@ EXPORTS = [
     "hlf_abi_version", "hlf_build_interp_operator", "hlf_create", "hlf_destroy", "hlf_last_error",
     "hlf_num_nodes", "hlf_num_coeffs", "hlf_set_field", "hlf_get_field", "hlf_set_coeff",
     "hlf_set_times", "hlf_get_times", "hlf_set_dt", "hlf_advance_p", "hlf_advance_v", "hlf_step",
-    "hlf_advance_n", "hlf_advance_p_indexed", "hlf_advance_v_indexed", "hlf_poll_finite", "hlf_clear_finite", "hlf_synchronize", "hlf_field_device",
+    "hlf_advance_n", "hlf_advance_p_indexed", "hlf_advance_v_indexed", "hlf_advance_layers", "hlf_commit_half",
+    "hlf_poll_finite", "hlf_clear_finite", "hlf_synchronize", "hlf_field_device",
     "hlf_fill_separable", "hlf_zero_field", "hlf_halo_send_ptr", "hlf_halo_recv_ptr",
     "hlf_launch_count", "hlf_kernel_variant", "hlf_set_kernel_variant",
 ]
@@ -80,6 +81,8 @@ def lib() -> C.CDLL:
         "hlf_advance_n": ([S, C.c_int, C.c_int], st),
         "hlf_advance_p_indexed": ([S, C.c_int], st),
         "hlf_advance_v_indexed": ([S, C.c_int], st),
+        "hlf_advance_layers": ([S, C.c_int, C.c_int, C.c_int, C.c_int], st),
+        "hlf_commit_half": ([S, C.c_int], st),
         "hlf_poll_finite": ([S, C.POINTER(C.c_int)], st),
         "hlf_clear_finite": ([S], st),
         "hlf_synchronize": ([S], st),

@@ -235,7 +235,10 @@ void fill_weights(const hlf_solver* s, hlfk::HalfKind kind, HalfParams& P) {
   P.av = s->av;
 }
 
-hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step) {
+// zlo/zhi: target layers [zlo, zhi) of a 3D half step (-1: all).  A range is
+// the full launch with both field bases shifted by zlo layers, so every kernel
+// runs it unchanged.
+hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0, int zhi = -1) {
   hlf_status st = fill_ghosts(s, kind == hlfk::PRE);
   if (st != HLF_OK) return st;
   HalfParams P;
@@ -267,6 +270,17 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step) {
   P.c_layer = s->plane[tf] * s->E;
   P.step = step;
   P.flag = s->flag;
+  if (zhi < 0) zhi = P.tNz;
+  if (zlo < 0 || zhi > P.tNz || zlo > zhi || (s->d != 3 && (zlo != 0 || zhi != P.tNz)))
+    return fail(s, HLF_INVALID_ARGUMENT, "layer range outside the target field (ranges are 3D only)");
+  if (zlo == zhi) return HLF_OK;
+  if (zlo > 0 || zhi < P.tNz) {
+    for (int c = 0; c < 3; ++c)
+      if (P.src[c]) P.src[c] += static_cast<int64_t>(zlo) * P.s_layer;
+    if (P.coeff) P.coeff += static_cast<int64_t>(zlo) * P.c_layer;
+    P.t_zoff += zlo;
+    P.tNz = zhi - zlo;
+  }
   int launched = -1;
   if (s->variant == 1 && !s->variable && s->d == 3 && hlfk::tiled3d_supported(s->m))
     launched = hlfk::launch_half_tiled3d(s->m, kind, P, s->stream);
@@ -499,6 +513,23 @@ hlf_status hlf_advance_v_indexed(hlf_solver* s, int step_index) {
   hlf_status st = launch_half(s, hlfk::VEL, step_index);
   if (st != HLF_OK) return st;
   s->t_v += s->dt;
+  return HLF_OK;
+}
+
+hlf_status hlf_advance_layers(hlf_solver* s, int half, int step_index, int z_begin, int z_end) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (half != 0 && half != 1) return fail(s, HLF_INVALID_ARGUMENT, "half must be 0 (pressure) or 1 (velocity)");
+  if (s->variable && !s->coeff[half == 0 ? HLF_PRIMARY : HLF_DUAL])
+    return fail(s, HLF_CONFIG_ERROR, "ap jets not set");
+  cudaSetDevice(s->device);
+  return launch_half(s, half == 0 ? hlfk::PRE : hlfk::VEL, step_index, z_begin, z_end);
+}
+
+hlf_status hlf_commit_half(hlf_solver* s, int half) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (half == 0) s->t_p += s->dt;
+  else if (half == 1) s->t_v += s->dt;
+  else return fail(s, HLF_INVALID_ARGUMENT, "half must be 0 (pressure) or 1 (velocity)");
   return HLF_OK;
 }
 

@@ -57,41 +57,70 @@ class HaloExchanger:
         self.pack = pack or (lambda kind: None)
         self.unpack = unpack or (lambda kind: None)
 
-    def _run(self, ops):
-        import torch.distributed as dist
-        reqs = dist.batch_isend_irecv(ops)
-        for r in reqs:
-            r.wait()
-
-    def exchange_p(self):
+    def _p_ops(self):
         # my p layer 0 is the previous rank's layer Kz; my layer Kz comes from the next rank
         import torch.distributed as dist
-        self.pack(0)
-        self._run([dist.P2POp(dist.isend, self.p_send, self.prev),
-                   dist.P2POp(dist.irecv, self.p_recv, self.next)])
-        self.unpack(0)
+        return [dist.P2POp(dist.isend, self.p_send, self.prev), dist.P2POp(dist.irecv, self.p_recv, self.next)]
 
-    def exchange_v(self):
+    def _v_ops(self):
         # my last v layer is the next rank's ghost z = -1; my ghost comes from the previous rank
         import torch.distributed as dist
-        self.pack(1)
         ops = []
         for c in range(3):
             ops.append(dist.P2POp(dist.isend, self.v_send[c], self.next))
             ops.append(dist.P2POp(dist.irecv, self.v_recv[c], self.prev))
-        self._run(ops)
-        self.unpack(1)
+        return ops
+
+    def start(self, kind: int):
+        """Issue the halo exchange of kind 0 (p) / 1 (v) and return its
+        requests.  With NCCL the transfers are ordered after the work already
+        queued on the current stream and run concurrently with what is
+        queued next; `finish` makes the current stream wait for them."""
+        import torch.distributed as dist
+        self.pack(kind)
+        return dist.batch_isend_irecv(self._p_ops() if kind == 0 else self._v_ops())
+
+    def finish(self, kind: int, reqs):
+        for r in reqs:
+            r.wait()
+        self.unpack(kind)
+
+    def exchange_p(self):
+        self.finish(0, self.start(0))
+
+    def exchange_v(self):
+        self.finish(1, self.start(1))
 
 
-def slab_step(solver, halo, step_index: int):
+def slab_step(solver, halo, step_index: int, overlap: bool = True):
     """One full leapfrog step of a slab (step_system order, stepper1d.cpp:168-172):
-    v halo -> advance_p -> p halo -> advance_v."""
-    if halo:
+    v halo -> advance_p -> p halo -> advance_v.
+
+    With `overlap` (and a backend that advances layer ranges) each halo is in
+    flight while the layers that do not need it are updated: the pressure half
+    step needs the v halo only for p layer 0, the velocity half step needs the
+    p halo only for v layer Kz-1.  p layer 0 is final before its halo is sent."""
+    if not halo:
+        solver.advance_p_indexed(step_index)
+        solver.advance_v_indexed(step_index)
+        return
+    if not (overlap and hasattr(solver, "advance_layers")):
         halo.exchange_v()
-    solver.advance_p_indexed(step_index)
-    if halo:
+        solver.advance_p_indexed(step_index)
         halo.exchange_p()
-    solver.advance_v_indexed(step_index)
+        solver.advance_v_indexed(step_index)
+        return
+    kz = solver.grid.K[2]
+    reqs = halo.start(1)
+    solver.advance_layers(0, step_index, 1, kz)      # p interior: no v halo needed
+    halo.finish(1, reqs)
+    solver.advance_layers(0, step_index, 0, 1)       # p layer 0 reads the v halo
+    solver.commit_half(0)
+    reqs = halo.start(0)                             # sends the final p layer 0
+    solver.advance_layers(1, step_index, 0, kz - 1)  # v interior: no p halo needed
+    halo.finish(0, reqs)
+    solver.advance_layers(1, step_index, kz - 1, kz)  # v layer Kz-1 reads the p halo
+    solver.commit_half(1)
 
 
 class SlabStepper:
@@ -140,7 +169,13 @@ class SlabStepper:
 
     # ---- stepping
     def step(self, step_index: int):
-        slab_step(self.solver, self.halo, step_index)
+        import torch
+        if self.stream is not None:
+            # NCCL orders the halo transfers after the solver stream's queued work
+            with torch.cuda.stream(self.stream):
+                slab_step(self.solver, self.halo, step_index)
+        else:
+            slab_step(self.solver, self.halo, step_index)
 
     def launch_count(self) -> int:
         return self.solver.launch_count

@@ -310,6 +310,15 @@ class Stepper:
     def advance_v_indexed(self, step_index: int):
         self._c(self._L.hlf_advance_v_indexed(self._h, step_index))
 
+    def advance_layers(self, half: int, step_index: int, z_begin: int, z_end: int):
+        """Half step (0 = pressure, 1 = velocity) over target layers
+        [z_begin, z_end) only, no time update (3D; z-slab overlap)."""
+        self._c(self._L.hlf_advance_layers(self._h, half, step_index, z_begin, z_end))
+
+    def commit_half(self, half: int):
+        """t_p (0) or t_v (1) += dt after a half step done in layer ranges."""
+        self._c(self._L.hlf_commit_half(self._h, half))
+
     def step_system(self, step_index: int):
         self._c(self._L.hlf_step(self._h, step_index))
 

@@ -292,11 +292,14 @@ def test_advance_n_equals_step_loop():
         assert np.array_equal(ga.get_field(f), gb.get_field(f))
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("m", [1, 3])
-def test_z_slabs_on_one_gpu_match_single_domain(m):
+def test_z_slabs_on_one_gpu_match_single_domain(m, overlap):
     """Two z-slab solvers (z_slab=True) on one GPU, halos copied through the
     hlf_halo_send/recv_ptr device views exactly as the NCCL exchanger does;
-    the result equals one periodic solver on the whole box."""
+    the result equals one periodic solver on the whole box.  With `overlap`
+    the slabs advance in layer ranges in distributed.slab_step's order: the
+    interior layers before the halo lands, the boundary layer after."""
     import torch
     from paper_1808_10481_b200.distributed import device_view
     K = [36, 4, 8]
@@ -321,23 +324,46 @@ def test_z_slabs_on_one_gpu_match_single_domain(m):
         ptr, cnt = s.halo_ptr(kind, comp, send)
         return device_view(ptr, cnt)
 
-    for i in range(3):
+    def v_halo():  # my ghost z=-1 <- previous rank's last layer
         for s in slabs:
             s.synchronize()
-        for r in range(2):  # v halo: my ghost z=-1 <- previous rank's last layer
+        for r in range(2):
             for c in range(3):
                 view(slabs[r], 1, c, False).copy_(view(slabs[(r - 1) % 2], 1, c, True))
         torch.cuda.synchronize()
+
+    def p_halo():  # my layer Kz <- next rank's layer 0
         for s in slabs:
-            s.advance_p_indexed(i)
             s.synchronize()
-        for r in range(2):  # p halo: my layer Kz <- next rank's layer 0
+        for r in range(2):
             view(slabs[r], 0, 0, False).copy_(view(slabs[(r + 1) % 2], 0, 0, True))
         torch.cuda.synchronize()
-        for s in slabs:
-            s.advance_v_indexed(i)
-            s.synchronize()
+
+    for i in range(3):
+        if overlap:
+            for s in slabs:
+                s.advance_layers(0, i, 1, kz)
+            v_halo()
+            for s in slabs:
+                s.advance_layers(0, i, 0, 1)
+                s.commit_half(0)
+                s.advance_layers(1, i, 0, kz - 1)
+            p_halo()
+            for s in slabs:
+                s.advance_layers(1, i, kz - 1, kz)
+                s.commit_half(1)
+                s.synchronize()
+        else:
+            v_halo()
+            for s in slabs:
+                s.advance_p_indexed(i)
+            p_halo()
+            for s in slabs:
+                s.advance_v_indexed(i)
+                s.synchronize()
         full.step_system(i)
+    for s in slabs:
+        assert s.times() == full.times()
     for f in range(4):
         ref = full.get_field(f).reshape(K[0], K[1], K[2], F)
         for r in range(2):
