@@ -133,6 +133,13 @@ hlf_status hlf_field_device(hlf_solver* s, int field, double** dev_ptr, int64_t*
 hlf_status hlf_fill_separable(hlf_solver* s, int field, double amp, const double* w,
                               const double* phase);
 hlf_status hlf_zero_field(hlf_solver* s, int field);
+/* On-device error accessor (the nodal counterpart of l2_error_1d/2d,
+   analysis.cpp:241-285, for separable trig data as filled by
+   hlf_fill_separable): rms over the field's nodes of value - exact, and the
+   max over nodes and scaled jet coefficients of |jet - exact jet|.
+   Synchronous; no state download (convergence sweeps stay on the device). */
+hlf_status hlf_error_separable(hlf_solver* s, int field, double amp, const double* w, const double* phase,
+                               double* rms_value, double* max_jet);
 
 /* --- z-slab halos (multi-GPU; z_slab = 1) -------------------------------- */
 /* The velocity half step reads p layer Kz (the next rank's layer 0); the

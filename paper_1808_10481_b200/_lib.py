@@ -23,7 +23,7 @@ EXPORTS = [
     "hlf_set_times", "hlf_get_times", "hlf_set_dt", "hlf_advance_p", "hlf_advance_v", "hlf_step",
     "hlf_advance_n", "hlf_advance_p_indexed", "hlf_advance_v_indexed", "hlf_advance_layers", "hlf_commit_half",
     "hlf_poll_finite", "hlf_clear_finite", "hlf_synchronize", "hlf_field_device",
-    "hlf_fill_separable", "hlf_zero_field", "hlf_halo_send_ptr", "hlf_halo_recv_ptr",
+    "hlf_fill_separable", "hlf_error_separable", "hlf_zero_field", "hlf_halo_send_ptr", "hlf_halo_recv_ptr",
     "hlf_launch_count", "hlf_kernel_variant", "hlf_set_kernel_variant",
 ]
 
@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
                               C.POINTER(C.c_int)], st),
         "hlf_fill_separable": ([S, C.c_int, C.c_double, _dp, _dp], st),
         "hlf_zero_field": ([S, C.c_int], st),
+        "hlf_error_separable": ([S, C.c_int, C.c_double, _dp, _dp, _dp, _dp], st),
         "hlf_halo_send_ptr": ([S, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)], st),
         "hlf_halo_recv_ptr": ([S, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)], st),
         "hlf_launch_count": ([S], C.c_int64),

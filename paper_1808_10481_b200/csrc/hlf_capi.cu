@@ -40,6 +40,8 @@ struct hlf_solver {
   double* coeff[2] = {nullptr, nullptr};
   int* flag = nullptr;
   int* flag_host = nullptr;
+  double* errbuf = nullptr;     // hlf_error_separable accumulator (device) and its host copy
+  double* errbuf_host = nullptr;
   double* staging = nullptr;
   size_t staging_bytes = 0;
   int64_t launches = 0;
@@ -416,6 +418,8 @@ void hlf_destroy(hlf_solver* s) {
     if (c) cudaFree(c);
   if (s->flag) cudaFree(s->flag);
   if (s->flag_host) cudaFreeHost(s->flag_host);
+  if (s->errbuf) cudaFree(s->errbuf);
+  if (s->errbuf_host) cudaFreeHost(s->errbuf_host);
   if (s->staging) cudaFree(s->staging);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -625,6 +629,46 @@ hlf_status hlf_fill_separable(hlf_solver* s, int field, double amp, const double
   }
   s->launches += hlfk::launch_fill(P, s->stream);
   HLF_CUDA(s, cudaGetLastError());
+  return HLF_OK;
+}
+
+hlf_status hlf_error_separable(hlf_solver* s, int field, double amp, const double* w, const double* phase,
+                               double* rms_value, double* max_jet) {
+  if (!s || !valid_field(s, field) || !w || !phase || !rms_value || !max_jet)
+    return fail(s, HLF_INVALID_ARGUMENT, "bad argument");
+  cudaSetDevice(s->device);
+  if (!s->errbuf) {
+    HLF_CUDA(s, cudaMalloc(&s->errbuf, 2 * sizeof(double)));
+    HLF_CUDA(s, cudaMallocHost(&s->errbuf_host, 2 * sizeof(double)));
+  }
+  hlfk::FillParams P;
+  std::memset(&P, 0, sizeof(P));
+  const int* N = s->nodes_of(field);
+  P.dst = s->field[field];
+  P.layer = s->layer_stride(field);
+  P.coef = s->plane[field];
+  P.Nx = N[0];
+  P.Ny = N[1];
+  P.Nz = N[2];
+  P.zoff = s->zoff(field);
+  P.d = s->d;
+  P.n1 = s->n1;
+  P.h = s->h;
+  P.amp = amp;
+  P.err = s->errbuf;
+  for (int ax = 0; ax < 3; ++ax) {
+    P.x0[ax] = s->x_min[ax] + (field == 0 ? 0.0 : 0.5 * s->h);
+    P.w[ax] = ax < s->d ? w[ax] : 0.0;
+    P.phase[ax] = ax < s->d ? phase[ax] : 0.0;
+  }
+  HLF_CUDA(s, cudaMemsetAsync(s->errbuf, 0, 2 * sizeof(double), s->stream));
+  s->launches += hlfk::launch_error(P, s->stream);
+  HLF_CUDA(s, cudaGetLastError());
+  HLF_CUDA(s, cudaMemcpyAsync(s->errbuf_host, s->errbuf, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+  const double nodes = static_cast<double>(N[0]) * N[1] * N[2];
+  *rms_value = std::sqrt(s->errbuf_host[0] / nodes);
+  *max_jet = s->errbuf_host[1];
   return HLF_OK;
 }
 

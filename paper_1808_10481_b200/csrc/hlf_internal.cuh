@@ -54,6 +54,7 @@ struct FillParams {
   double x0[3];                 // coordinate of node 0 along each axis
   double h, amp;
   double w[3], phase[3];
+  double* err;                  // launch_error: [sum of squared value errors, max |jet error|]
 };
 
 // launchers (return the number of kernels launched)
@@ -64,6 +65,8 @@ bool tiled3d_supported(int m);
 int launch_half_tiled2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
 bool tiled2d_supported(int m);
 int launch_fill(const FillParams& p, cudaStream_t st);
+// field - amp prod sin_jet -> err[0] += sum of squared value errors, err[1] = max |jet error|
+int launch_error(const FillParams& p, cudaStream_t st);
 namespace v5 {
 // 16-warp tiled kernel, m = 3 (kernels_tiled3d_v5.cu)
 int launch(HalfKind kind, const HalfParams& p, cudaStream_t st);

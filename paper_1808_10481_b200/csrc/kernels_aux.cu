@@ -41,6 +41,57 @@ __global__ void fill_separable(const __grid_constant__ FillParams P) {
   }
 }
 
+// Nodal error against separable trig data (the on-device counterpart of the
+// host accessors l2_error_1d/2d, analysis.cpp:241-285, at the nodes instead of
+// Gauss points): err[0] += sum over nodes of (value - exact)^2, err[1] = max
+// over nodes and scaled jet coefficients of |jet - exact jet|.
+__global__ void separable_error(const __grid_constant__ FillParams P) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = static_cast<int64_t>(P.Nx) * P.Ny * P.Nz;
+  double sq = 0.0, mx = 0.0;
+  if (tid < total) {
+    const int ix = static_cast<int>(tid % P.Nx);
+    const int64_t r = tid / P.Nx;
+    const int iy = static_cast<int>(r % P.Ny);
+    const int iz = static_cast<int>(r / P.Ny);
+    const int idx[3] = {ix, iy, iz};
+    const double pi = 3.141592653589793238462643383279502884;
+    double jet[3][kMaxM + 1];
+    for (int ax = 0; ax < 3; ++ax) {
+      double base = ax == 0 ? P.amp : 1.0;
+      const double x0 = P.x0[ax] + idx[ax] * P.h;
+      for (int i = 0; i < P.n1; ++i) {
+        jet[ax][i] = ax < P.d ? base * sin(P.w[ax] * x0 + P.phase[ax] + i * pi / 2.0) : (i == 0 ? base : 0.0);
+        base *= P.h * P.w[ax] / static_cast<double>(i + 1);
+      }
+    }
+    const int F = P.d == 1 ? P.n1 : (P.d == 2 ? P.n1 * P.n1 : P.n1 * P.n1 * P.n1);
+    const double* base = P.dst + static_cast<int64_t>(P.zoff + iz) * P.layer + static_cast<int64_t>(iy) * P.Nx + ix;
+    for (int f = 0; f < F; ++f) {
+      int a[3] = {0, 0, 0};
+      int e = f;
+      for (int ax = P.d - 1; ax >= 0; --ax) {
+        a[ax] = e % P.n1;
+        e /= P.n1;
+      }
+      double v = 1.0;
+      for (int ax = P.d - 1; ax >= 0; --ax) v *= jet[ax][a[ax]];
+      const double dv = base[f * P.coef] - v;
+      if (f == 0) sq = dv * dv;
+      mx = fmax(mx, fabs(dv));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    sq += __shfl_down_sync(0xffffffffu, sq, o);
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(P.err, sq);
+    // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(P.err + 1), static_cast<unsigned long long>(__double_as_longlong(mx)));
+  }
+}
+
 // dst plane (coef-major [F][plane]) = sigma * (-1)^{a_z} src, a_z = last index
 __global__ void mirror_layer(double* dst, const double* src, int64_t plane, int n1, int F,
                              double sigma) {
@@ -73,6 +124,13 @@ __global__ void aos_soa(const double* __restrict__ in, double* __restrict__ out,
 unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 }  // namespace
+
+int launch_error(const FillParams& p, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(p.Nx) * p.Ny * p.Nz;
+  if (total == 0) return 0;
+  separable_error<<<blocks_for(total, 128), 128, 0, st>>>(p);
+  return 1;
+}
 
 int launch_fill(const FillParams& p, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(p.Nx) * p.Ny * p.Nz;

@@ -358,6 +358,15 @@ class Stepper:
         p3 = (C.c_double * 3)(*(list(phase) + [0.0] * (3 - len(phase))))
         self._c(self._L.hlf_fill_separable(self._h, f, amp, w3, p3))
 
+    def error_separable(self, f: int, amp: float, w: Sequence[float], phase: Sequence[float]):
+        """(rms value error, max scaled-jet error) of field f against
+        amp * prod sin(w x + phase), computed on the device."""
+        w3 = (C.c_double * 3)(*(list(w) + [0.0] * (3 - len(w))))
+        p3 = (C.c_double * 3)(*(list(phase) + [0.0] * (3 - len(phase))))
+        rms, mx = C.c_double(), C.c_double()
+        self._c(self._L.hlf_error_separable(self._h, f, amp, w3, p3, C.byref(rms), C.byref(mx)))
+        return rms.value, mx.value
+
     def zero_field(self, f: int):
         self._c(self._L.hlf_zero_field(self._h, f))
 

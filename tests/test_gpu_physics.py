@@ -126,3 +126,28 @@ def test_3d_m3_accuracy():
     # the error levels instead
     es = [mode_error(3, 3, K) for K in (8, 16, 32)]
     assert es[0] < 1e-8 and es[1] < 1e-9 and es[2] < 1e-12, es
+
+
+@pytest.mark.parametrize("d,m", [(1, 3), (2, 2), (3, 3)])
+def test_error_accessor_matches_host(d, m):
+    # hlf_error_separable (device) == the same nodal norms computed on the host
+    # from downloaded jets and the oracle's exact jets (add_separable)
+    K = [12, 10, 8][:d]
+    h = 2.0 / K[0]
+    g = H.Stepper(H.Grid([-1.0] * d, h, tuple(K)), m)
+    pi = math.pi
+    w = [pi] * d
+    g.fill_separable(0, 1.0, w, [0.0] * d)
+    for c in range(1, d + 1):
+        g.fill_separable(c, -0.3, w, [pi / 2 if a == c - 1 else 0.0 for a in range(d)])
+    g.set_times(0.0, 0.01, 0.02)
+    g.advance_n(5)
+    n1 = m + 1
+    for f, amp, ph in ((0, 0.97, [0.0] * d), (1, -0.31, [pi / 2] + [0.0] * (d - 1))):
+        rms, mx = g.error_separable(f, amp, w, ph)
+        got = g.get_field(f)
+        ex = np.zeros_like(got)
+        O.add_separable(d, list(K), [-1.0] * d, h, 0.0 if f == 0 else 0.5, n1, amp, w, ph, ex)
+        diff = got - ex
+        assert rms == pytest.approx(math.sqrt((diff[:, 0] ** 2).mean()), rel=1e-12, abs=1e-300)
+        assert mx == pytest.approx(np.abs(diff).max(), rel=1e-12, abs=1e-300)
