@@ -29,13 +29,16 @@
 #include <type_traits>
 #include <utility>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "hlf_internal.cuh"
 
 namespace hlfk {
 namespace {
 
 constexpr int TXC = 32;         // cells per CTA row (= lanes)
-constexpr int RAWX = TXC + 1;   // source nodes per row
+constexpr int RAWX = TXC + 2;   // source row stride: 33 nodes used, 34 = 17 x 16 B (TMA row copies)
 constexpr int NWARP = 8;
 constexpr int NTHREADS = NWARP * 32;
 constexpr int ZC = 128;         // target layers per CTA (128: +0.5 % over 64 at m = 3, 256: -1 %)
@@ -45,6 +48,9 @@ template <int MM>
 struct Cfg {
   static constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1 * n1, nh = n / 2, jh = (n1 + 1) / 2;
   static constexpr int RAW = F * 2 * RAWX;
+  // raw stage stride: one spare double each side for the pre shift, rounded
+  // to 128 B (TMA tensor destinations must be 128 B aligned)
+  static constexpr int RAWS = (RAW + 2 + 15) / 16 * 16;
   static constexpr int RING = n * n * n1 * TXC;
   // NT: 3 = velocity half (three targets), 1 = one pressure divergence term,
   // 2 = merged V_x + V_y pressure launch (two raw sources, one target; m = 3)
@@ -62,10 +68,11 @@ struct Cfg {
   template <int NT>
   static constexpr int NBUF = (NT == 1 && MM < 3) ? 2 : 1;
   template <int NT>
-  static constexpr int SMEM_DOUBLES = NRAW<NT> * RAW + 2 * RING + TGT<NT>;
+  static constexpr int SMEM_DOUBLES = NRAW<NT> * RAWS + 2 * RING + TGT<NT>;
 };
 
 struct TParams {
+  CUtensorMap tmap[2];             // raw source tensors [layer][coef][y][x] for TMA box loads
   double ML[kMaxN * (kMaxM + 1)];  // s! * M[s][l], l < m+1 (left block), row-major [s][l]
   double GM[kMaxB];                // G_k * k!/b!, indexed by bindex(b)
   double IF[kMaxM + 1];            // 1/o!
@@ -82,6 +89,7 @@ struct TParams {
   int pre;                         // 1: source is the dual family (x0 - 1 shift, mirrors)
   int comp;                        // source component (mirror parity), PRE only
   int step;
+  int tma;                         // strides allow 16 B aligned TMA row copies
   int* flag;
 };
 
@@ -112,6 +120,35 @@ __device__ __forceinline__ void cp_async8_ordered(double* smem, const double* gm
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// one tensor box global -> shared (x, y, coefficient plane 0, layer), completing on the mbarrier
+__device__ __forceinline__ void tma_box(double* smem, const CUtensorMap* map, int x, int y, int layer, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(0), "r"(layer),
+      "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 
 #include "tiled3d_gen.cuh"
@@ -187,9 +224,16 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   constexpr bool MX = NT == 2;                // merged V_x + V_y pressure launch
   constexpr int NTT = G::template NTGT<NT>;   // target fields
   static_assert(!MX || MM == 3, "merged pressure launch is generated for m = 3");
-  extern __shared__ __align__(16) double smem[];
-  double* rawbuf = smem;                      // NB raw stages (MX: raw V_x, raw V_y)
-  double* ring0 = rawbuf + G::template NRAW<NT> * G::RAW;
+  extern __shared__ __align__(128) double smem_raw[];
+  // TMA tensor destinations must be 128 B aligned: align the base explicitly
+  // (the launch requests 128 B of slack)
+  // (offset arithmetic on smem_raw keeps the accesses LDS/STS; a pointer
+  // rebuilt from an integer would turn them into generic loads)
+  double* smem = smem_raw + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 127u)) & 127u) / 8u;
+  // raw stages (MX: raw V_x, raw V_y); node index 0 of a row sits at
+  // stage base + pre so that TMA row copies start on a 16 B boundary
+  double* rawbuf = smem + P.pre;
+  double* ring0 = smem + G::template NRAW<NT> * G::RAWS;
   double* ring1 = ring0 + G::RING;
   double* tgs = ring1 + G::RING;              // target stage [t][f][cell], lane-private entries
   double* raw = rawbuf;
@@ -235,15 +279,46 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   const int64_t yo0 = static_cast<int64_t>(ymap(0, my0)) * P.sNx;
   const int64_t yo1 = static_cast<int64_t>(ymap(1, my1)) * P.sNx;
   const bool walls = __syncthreads_or(mx_lane || mx_last || my0 || my1);
+  __shared__ __align__(8) uint64_t rawbar[2];
+  uint32_t rphase = 0;
+  // TMA boxes need: no x wrap / mirror inside the row, the two source rows
+  // consecutive and unmirrored
+  const bool tma_rows = P.tma && (P.pre ? (x0 >= 2 && x0 + TXC <= P.sNx) : (x0 + RAWX <= P.sNx)) &&
+                        !__syncthreads_or(mx_lane || mx_last) && (P.pre ? x0 - 1 + TXC < P.K[0] : true) && !my0 &&
+                        !my1 && yo1 == yo0 + P.sNx;
+  if (tid == 0) {
+    mbar_init(&rawbar[0], 1);
+    mbar_init(&rawbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
   constexpr int ROWS = 2 * F;
+  // Interior CTAs (no wrap or mirror along x) load every raw row with one TMA
+  // bulk copy (34 nodes = 272 B, 16 B aligned) completing on an mbarrier;
+  // boundary CTAs and unaligned strides use per-node cp.async.
   auto issue_raw = [&](int layer) {
 #ifdef HLF_EXP_NORAW
     cp_async_commit();
     return;
 #endif
+    if (tma_rows) {
+      // one 4D box (34 nodes x 2 rows x F coefficients x 1 layer) per source
+      const int stage = NB == 2 ? (layer & 1) : 0;
+      if (tid == 0) {
+        constexpr int NS = MX ? 2 : 1;
+        mbar_expect_tx(&rawbar[stage], NS * G::RAW * 8);
+        fence_proxy_async();
+#pragma unroll
+        for (int si = 0; si < NS; ++si)
+          tma_box(rawbuf + (MX ? si : stage) * G::RAWS - P.pre, &P.tmap[si], x0 - 2 * P.pre, ty - P.pre, layer,
+                  &rawbar[stage]);
+      }
+      cp_async_commit();  // empty group: keeps the per-thread group pattern
+      return;
+    }
 #pragma unroll
    for (int si = 0; si < (MX ? 2 : 1); ++si) {
-    double* raw = rawbuf + (MX ? si : (NB == 2 ? (layer & 1) : 0)) * G::RAW;
+    double* raw = rawbuf + (MX ? si : (NB == 2 ? (layer & 1) : 0)) * G::RAWS;
     const double* base = (si ? P.src2 : P.src) + static_cast<int64_t>(layer) * P.s_layer;
     if constexpr (ROWS % NWARP == 0) {
       // row r = warp + 8 i: coefficient plane (warp >> 1) + 4 i, source row warp & 1
@@ -286,16 +361,22 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   auto fix_walls = [&]() {
     if constexpr (MX) {
       fix_walls_buf(rawbuf, 0);
-      fix_walls_buf(rawbuf + G::RAW, 1);
+      fix_walls_buf(rawbuf + G::RAWS, 1);
     } else {
       fix_walls_buf(raw, P.comp);
     }
   };
-  auto finish_raw = [&]() {
+  auto finish_raw = [&](int layer) {
     cp_async_wait_group1();  // this thread's raw(k+1) landed; its targets(k) may be in flight
+    if (tma_rows) {
+      const int stage = NB == 2 ? (layer & 1) : 0;
+      mbar_wait(&rawbar[stage], (rphase >> stage) & 1);
+      rphase ^= 1u << stage;
+    }
     if (walls) {
       __syncthreads();
       fix_walls();
+      if (tma_rows) fence_proxy_async();  // generic writes before the next TMA refill of this stage
     }
     __syncthreads();
   };
@@ -358,8 +439,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
 #pragma unroll 1
   for (int k = k0 - 1; k < k1; ++k) {
     const bool work = k >= k0;
-    raw = rawbuf + (NB == 2 ? ((k + 1) & 1) : 0) * G::RAW;
-    finish_raw();  // raw(k+1) landed; every warp left the previous Z + CK stage
+    raw = rawbuf + (NB == 2 ? ((k + 1) & 1) : 0) * G::RAWS;
+    finish_raw(k + 1);  // raw(k+1) landed; every warp left the previous Z + CK stage
     if (NB == 2) {
       if (k + 1 < k1) issue_raw(k + 2); else cp_async_commit();
     }
@@ -368,7 +449,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       const int lz = warp >> 1;
       double* wb = rn + lz * TXC + lane;
       const double* rbx = rawbuf + lz * 2 * RAWX + lane;
-      const double* rby = rbx + G::RAW;
+      const double* rby = rbx + G::RAWS;
 #ifndef HLF_XY_RMW
       if (warp & 1) m3_xy_px1_vxy(P, rbx, rby, wb); else m3_xy_px0_vxy(P, rbx, rby, wb);
 #else
@@ -460,10 +541,45 @@ double host_fact(int k) {
   return r;
 }
 
+// Driver entry point for cuTensorMapEncodeTiled (no libcuda link dependency)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// raw source tensor [layer][coef][y][x] with box (RAWX, 2, F, 1); false if not encodable
+template <int MM>
+bool encode_raw_map(CUtensorMap* map, const double* base, const TParams& T, int layers) {
+  auto enc = tensor_map_encoder();
+  if (enc == nullptr || base == nullptr || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  constexpr int n1 = MM + 1, F = n1 * n1 * n1;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(T.sNx), static_cast<cuuint64_t>(T.sNy),
+                              static_cast<cuuint64_t>(F), static_cast<cuuint64_t>(layers)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(T.sNx) * 8, static_cast<cuuint64_t>(T.s_plane) * 8,
+                                 static_cast<cuuint64_t>(T.s_layer) * 8};
+  const cuuint32_t box[4] = {RAWX, 2, F, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int MM, int NT>
-int launch_one(const TParams& T, cudaStream_t st) {
+int launch_one(TParams T, cudaStream_t st) {
+  if (T.tma) {
+    const int layers = T.tNz + 3;
+    T.tma = encode_raw_map<MM>(&T.tmap[0], T.src, T, layers) &&
+            (NT != 2 || encode_raw_map<MM>(&T.tmap[1], T.src2, T, layers));
+  }
   using G = Cfg<MM>;
-  const size_t smem = sizeof(double) * G::template SMEM_DOUBLES<NT>;
+  const size_t smem = sizeof(double) * G::template SMEM_DOUBLES<NT> + 128;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tiled3d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -506,6 +622,8 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.bnd[1] = p.bnd[1];
   T.step = p.step;
   T.flag = p.flag;
+  // TMA boxes: 16 B aligned strides and bases (checked again per tensor map)
+  T.tma = std::getenv("HLF_NO_TMA") == nullptr && p.s_layer % 2 == 0 && p.s_coef % 2 == 0 && p.sNx % 2 == 0;
   if (kind == VEL) {
     T.pre = 0;
     T.comp = 0;

@@ -25,7 +25,7 @@ from __future__ import annotations
 import os
 
 TXC = 32
-RAWX = TXC + 1
+RAWX = TXC + 2  # raw row stride: 33 nodes used, 34 for 16 B aligned TMA row copies
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(HERE, "..", "paper_1808_10481_b200", "csrc", "tiled3d_gen.cuh")
 
