@@ -73,6 +73,7 @@ struct Cfg {
 
 struct TParams {
   CUtensorMap tmap[2];             // raw source tensors [layer][coef][y][x] for TMA box loads
+  CUtensorMap tmapT[3];            // target tensors, box (32 cells, 1 row, F, 1 layer)
   double ML[kMaxN * (kMaxM + 1)];  // s! * M[s][l], l < m+1 (left block), row-major [s][l]
   double GM[kMaxB];                // G_k * k!/b!, indexed by bindex(b)
   double IF[kMaxM + 1];            // 1/o!
@@ -90,6 +91,7 @@ struct TParams {
   int comp;                        // source component (mirror parity), PRE only
   int step;
   int tma;                         // strides allow 16 B aligned TMA row copies
+  int tma_t;                       // target tensor maps encoded
   int* flag;
 };
 
@@ -280,7 +282,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   const int64_t yo1 = static_cast<int64_t>(ymap(1, my1)) * P.sNx;
   const bool walls = __syncthreads_or(mx_lane || mx_last || my0 || my1);
   __shared__ __align__(8) uint64_t rawbar[2];
-  uint32_t rphase = 0;
+  __shared__ __align__(8) uint64_t tgtbar;
+  uint32_t rphase = 0, tphase = 0;
   // TMA boxes need: no x wrap / mirror inside the row, the two source rows
   // consecutive and unmirrored
   const bool tma_rows = P.tma && (P.pre ? (x0 >= 2 && x0 + TXC <= P.sNx) : (x0 + RAWX <= P.sNx)) &&
@@ -289,6 +292,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   if (tid == 0) {
     mbar_init(&rawbar[0], 1);
     mbar_init(&rawbar[1], 1);
+    mbar_init(&tgtbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   // groups: every iteration commits [raw(k+2)] then [targets(k+1)], so
   // wait_group 1 at the top (raw) and before the epilogue (targets) suffices.
   auto issue_own_targets = [&](int kk) {
-    if (zactive) {
+    if (zactive && !P.tma_t) {
       const int64_t ob = static_cast<int64_t>(P.t_zoff + kk) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
 #pragma unroll 1
       for (int t = 0; t < NTT; ++t) {
@@ -441,6 +445,13 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     const bool work = k >= k0;
     raw = rawbuf + (NB == 2 ? ((k + 1) & 1) : 0) * G::RAWS;
     finish_raw(k + 1);  // raw(k+1) landed; every warp left the previous Z + CK stage
+    if (P.tma_t && work && tid == 0) {
+      // targets of layer k, one box per target field; consumed after the Z + CK sums
+      mbar_expect_tx(&tgtbar, NTT * F * TXC * 8);
+      fence_proxy_async();
+#pragma unroll
+      for (int t = 0; t < NTT; ++t) tma_box(tgs + t * F * TXC, &P.tmapT[t], x0, ty, P.t_zoff + k, &tgtbar);
+    }
     if (NB == 2) {
       if (k + 1 < k1) issue_raw(k + 2); else cp_async_commit();
     }
@@ -480,7 +491,12 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       if constexpr (V7) v7_m3_z(ro + cbase, rn + cbase, cz, zg, pt);
       else z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
       const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
-      cp_async_wait_group1();  // this lane's targets(k) landed; raw(k+2) may be in flight
+      if (P.tma_t) {
+        mbar_wait(&tgtbar, tphase);
+        tphase ^= 1u;
+      } else {
+        cp_async_wait_group1();  // this lane's targets(k) landed; raw(k+2) may be in flight
+      }
 #pragma unroll 1
       for (int t = 0; t < NTT; ++t) {
         const int c = MX ? -1 : (NT == 3 ? t : P.comp);  // -1: shifts already in the XY rows
@@ -524,7 +540,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       }
     }
 #ifndef HLF_EXP_NOTGT
-    if (k + 1 < k1) issue_own_targets(k + 1); else cp_async_commit();
+    if (k + 1 < k1 && !P.tma_t) issue_own_targets(k + 1); else cp_async_commit();
 #else
     cp_async_commit();
 #endif
@@ -571,8 +587,32 @@ bool encode_raw_map(CUtensorMap* map, const double* base, const TParams& T, int 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// target tensor [layer][coef][y][x] with box (TXC, 1, F, 1); out-of-range cells are zero-filled
+template <int MM>
+bool encode_tgt_map(CUtensorMap* map, const double* base, const TParams& T, int layers) {
+  auto enc = tensor_map_encoder();
+  if (enc == nullptr || base == nullptr || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  if (T.tNx % 2 || T.t_plane % 2 || T.t_layer % 2) return false;
+  constexpr int n1 = MM + 1, F = n1 * n1 * n1;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(T.tNx), static_cast<cuuint64_t>(T.tNy),
+                              static_cast<cuuint64_t>(F), static_cast<cuuint64_t>(layers)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(T.tNx) * 8, static_cast<cuuint64_t>(T.t_plane) * 8,
+                                 static_cast<cuuint64_t>(T.t_layer) * 8};
+  const cuuint32_t box[4] = {TXC, 1, F, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int MM, int NT>
 int launch_one(TParams T, cudaStream_t st) {
+  {
+    constexpr int NTT = Cfg<MM>::template NTGT<NT>;
+    bool ok = T.tma_t != 0;
+    for (int t = 0; t < NTT && ok; ++t) ok = encode_tgt_map<MM>(&T.tmapT[t], T.dst[t], T, T.t_zoff + T.tNz + 2);
+    T.tma_t = ok;
+  }
   if (T.tma) {
     const int layers = T.tNz + 3;
     T.tma = encode_raw_map<MM>(&T.tmap[0], T.src, T, layers) &&
@@ -624,6 +664,7 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.flag = p.flag;
   // TMA boxes: 16 B aligned strides and bases (checked again per tensor map)
   T.tma = std::getenv("HLF_NO_TMA") == nullptr && p.s_layer % 2 == 0 && p.s_coef % 2 == 0 && p.sNx % 2 == 0;
+  T.tma_t = std::getenv("HLF_NO_TMA_T") == nullptr;
   if (kind == VEL) {
     T.pre = 0;
     T.comp = 0;
