@@ -20,6 +20,9 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "hlf_internal.cuh"
 
 namespace hlfk {
@@ -27,13 +30,15 @@ namespace t2 {
 namespace {
 
 constexpr int TXC = 32;
-constexpr int RAWX = TXC + 1;
+constexpr int RAWX = TXC + 2;  // 33 source nodes used; 34 keeps TMA rows 16 B multiples
 constexpr int NWARP = 4;
 constexpr int NTHREADS = NWARP * 32;
 constexpr int ZC = 64;
 constexpr int kMaxB2 = 15;  // |b| <= 4 in 2D
 
 struct T2Params {
+  CUtensorMap tmap[2];             // raw source tensors [coef][y][x], box (RAWX, 1, F)
+  CUtensorMap tmapT[2];            // target tensors, box (TXC, 1, F)
   double ML[kMaxN * (kMaxM + 1)];  // s! M[s][l] (left block)
   double GM[kMaxB2];               // G_k k!/b!
   const double* src;
@@ -43,6 +48,7 @@ struct T2Params {
   int sNx, sNy, tNx, tNy;
   int K[2], bnd[2];
   int pre, comp, step;
+  int tma, tma_t;                  // tensor maps encoded (raw sources / targets)
   int* flag;
 };
 
@@ -53,6 +59,35 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// one tensor box (x, y, coefficient plane 0) global -> shared, completing on the mbarrier
+__device__ __forceinline__ void tma_box3(double* smem, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(0),
+      "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 template <int MM>
@@ -102,11 +137,14 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
   constexpr int NS = MX ? 2 : 1;       // raw sources
   constexpr int NTT = MX ? 1 : NT;     // target fields
   constexpr int RAW = F * RAWX;
+  constexpr int RAWS = (RAW + 2 + 15) / 16 * 16;  // raw stage stride (128 B multiple, pre-shift spare)
   constexpr int RING = n * n1 * TXC;
   constexpr int TGT = NTT * F * TXC;
-  extern __shared__ __align__(16) double smem[];
-  double* rawbuf = smem;               // [source][2 stages]
-  double* ring0 = rawbuf + 2 * NS * RAW;
+  extern __shared__ __align__(128) double smem_raw[];
+  // 128 B aligned base by offset arithmetic (keeps the accesses LDS/STS)
+  double* smem = smem_raw + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 127u)) & 127u) / 8u;
+  double* rawbuf = smem + P.pre;       // [source][2 stages]; node 0 of a row at stage base + pre
+  double* ring0 = smem + 2 * NS * RAWS;
   double* ring1 = ring0 + RING;
   double* ringb0 = ring1 + RING;       // MX: x-lines of V_y (ring A = ring0/1 holds V_x's)
   double* ringb1 = ringb0 + (MX ? RING : 0);
@@ -148,14 +186,38 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
   const int xo_lane = xmap(lane, mx_lane);
   const int xo_last = xmap(TXC, mx_last);
   const bool xwall = __syncthreads_or(mx_lane || mx_last);
+  // TMA rows: no x wrap / mirror inside the row (edge CTAs load per node)
+  const bool tma_rows = P.tma && !xwall && (P.pre ? (x0 >= 2 && x0 + TXC <= P.sNx && x0 - 1 + TXC < P.K[0])
+                                                  : (x0 + RAWX <= P.sNx && x0 + TXC < P.K[0]));
+  __shared__ __align__(8) uint64_t rawbar[2], tgtbar[2];
+  unsigned rphase = 0, tphase = 0;
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&rawbar[i], 1);
+      mbar_init(&tgtbar[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
 
   // source row sr (allocation row index of the source family) -> raw stage
   auto issue_raw = [&](int sr) {
     bool my;
     const int q = ymap(sr, my);
+    if (tma_rows) {
+      if (tid == 0) {
+        mbar_expect_tx(&rawbar[sr & 1], NS * RAW * 8);
+        fence_proxy_async();
+#pragma unroll
+        for (int si = 0; si < NS; ++si)
+          tma_box3(rawbuf + (si * 2 + (sr & 1)) * RAWS - P.pre, &P.tmap[si], x0 - 2 * P.pre, q, &rawbar[sr & 1]);
+      }
+      cp_async_commit();
+      return;
+    }
 #pragma unroll
     for (int si = 0; si < NS; ++si) {
-      double* raw = rawbuf + (si * 2 + (sr & 1)) * RAW;
+      double* raw = rawbuf + (si * 2 + (sr & 1)) * RAWS;
       const double* rowbase = (si ? P.src2 : P.src) + static_cast<int64_t>(q) * P.sNx;
       for (int f = warp; f < F; f += NWARP) cp_async8(raw + f * RAWX + lane, rowbase + f * P.s_plane + xo_lane);
       if (tid < F) cp_async8(raw + tid * RAWX + TXC, rowbase + tid * P.s_plane + xo_last);
@@ -168,7 +230,7 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
     (void)ymap(sr, my);
     if (!my && !xwall) return;
     for (int si = 0; si < NS; ++si) {
-      double* raw = rawbuf + (si * 2 + (sr & 1)) * RAW;
+      double* raw = rawbuf + (si * 2 + (sr & 1)) * RAWS;
       const int comp = MX ? si : P.comp;
       for (int e = tid; e < RAW; e += NTHREADS) {
         const int f = e / RAWX, sx = e - f * RAWX;
@@ -180,9 +242,20 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
         if (neg) raw[e] = -raw[e];
       }
     }
+    if (tma_rows) fence_proxy_async();  // generic writes before the next TMA refill of this stage
   };
   auto issue_targets = [&](int j) {
     double* tg = tgsbuf + (j & 1) * TGT;
+    if (P.tma_t) {
+      if (tid == 0) {
+        mbar_expect_tx(&tgtbar[j & 1], TGT * 8);
+        fence_proxy_async();
+#pragma unroll
+        for (int t = 0; t < NTT; ++t) tma_box3(tg + t * F * TXC, &P.tmapT[t], x0, j, &tgtbar[j & 1]);
+      }
+      cp_async_commit();
+      return;
+    }
     if (x0 + lane < P.tNx) {
       const int64_t rowoff = static_cast<int64_t>(j) * P.tNx + x0 + lane;
       for (int r = warp; r < NTT * F; r += NWARP) {
@@ -204,17 +277,21 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
     const bool work = j >= j0;
     const int snew = j + 1 - P.pre;  // source row entering the ring this iteration
     cp_async_wait_all();
+    if (tma_rows) {
+      mbar_wait(&rawbar[snew & 1], (rphase >> (snew & 1)) & 1);
+      rphase ^= 1u << (snew & 1);
+    }
     __syncthreads();
     fix_raw(snew);
     __syncthreads();
     if (j + 1 < j1) issue_raw(snew + 1);
     if (j + 1 < j1) issue_targets(j + 1);
-    const double* raw = rawbuf + (snew & 1) * RAW;
+    const double* raw = rawbuf + (snew & 1) * RAWS;
     if constexpr (MX) {
       // V_x with the shifted x rows into ring A, V_y into ring B
       for (int task = warp; task < 4 * n1; task += NWARP) {
         const int si = task >= 2 * n1, tk = task - si * 2 * n1, ly = tk >> 1, px = tk & 1;
-        if (si) x_task<MM>(px, P, raw + 2 * RAW + ly * RAWX + lane, rnb + ly * TXC + lane);
+        if (si) x_task<MM>(px, P, raw + 2 * RAWS + ly * RAWX + lane, rnb + ly * TXC + lane);
         else x_task_sh<MM>(px, P, raw + ly * RAWX + lane, rn + ly * TXC + lane);
       }
     } else {
@@ -224,6 +301,10 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
       }
     }
     __syncthreads();
+    if (work && P.tma_t) {
+      mbar_wait(&tgtbar[j & 1], (tphase >> (j & 1)) & 1);
+      tphase ^= 1u << (j & 1);
+    }
     if (work) {
       double* dptr[NTT];
       for (int t = 0; t < NTT; ++t) dptr[t] = P.dst[t] + static_cast<int64_t>(j) * P.tNx + x0 + lane;
@@ -249,11 +330,43 @@ double host_fact(int k) {
   return r;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// [coef][y][x] tensor, box (bx, 1, F); false if not encodable (alignment, no driver entry)
+bool encode_map(CUtensorMap* map, const double* base, int nx, int ny, int F, int64_t plane, int bx) {
+  auto enc = tensor_map_encoder();
+  if (enc == nullptr || base == nullptr || (reinterpret_cast<uintptr_t>(base) & 15) != 0 || nx % 2 || plane % 2)
+    return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(nx), static_cast<cuuint64_t>(ny), static_cast<cuuint64_t>(F)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(nx) * 8, static_cast<cuuint64_t>(plane) * 8};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(bx), 1, static_cast<cuuint32_t>(F)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int MM, int NT>
-int launch_one(const T2Params& T, cudaStream_t st) {
+int launch_one(T2Params T, cudaStream_t st) {
   constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1;
   constexpr int NS = NT == 3 ? 2 : 1, NTT = NT == 3 ? 1 : NT;
-  const size_t smem = sizeof(double) * (2 * NS * F * RAWX + 2 * NS * n * n1 * TXC + 2 * NTT * F * TXC);
+  constexpr int RAWS = (F * RAWX + 2 + 15) / 16 * 16;
+  const bool want = std::getenv("HLF_NO_TMA") == nullptr;
+  T.tma = want && encode_map(&T.tmap[0], T.src, T.sNx, T.sNy, F, T.s_plane, RAWX) &&
+          (NS == 1 || encode_map(&T.tmap[1], T.src2, T.sNx, T.sNy, F, T.s_plane, RAWX));
+  T.tma_t = want;
+  for (int t = 0; t < NTT && T.tma_t; ++t) T.tma_t = encode_map(&T.tmapT[t], T.dst[t], T.tNx, T.tNy, F, T.t_plane, TXC);
+  const size_t smem = sizeof(double) * (2 * NS * RAWS + 2 * NS * n * n1 * TXC + 2 * NTT * F * TXC) + 128;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tiled2d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

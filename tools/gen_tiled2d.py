@@ -19,7 +19,7 @@ import os
 from math import factorial
 
 TXC = 32
-RAWX = TXC + 1
+RAWX = TXC + 2  # 33 nodes used; 34 keeps TMA rows 16 B multiples
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(HERE, "..", "paper_1808_10481_b200", "csrc", "tiled2d_gen.cuh")
 
