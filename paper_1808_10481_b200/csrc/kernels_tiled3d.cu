@@ -41,7 +41,7 @@ constexpr int TXC = 32;         // cells per CTA row (= lanes)
 constexpr int RAWX = TXC + 2;   // source row stride: 33 nodes used, 34 = 17 x 16 B (TMA row copies)
 constexpr int NWARP = 8;
 constexpr int NTHREADS = NWARP * 32;
-constexpr int ZC = 128;         // target layers per CTA (128: +0.5 % over 64 at m = 3, 256: -1 %)
+constexpr int ZC = 64;          // target layers per CTA (with TMA loads: 64 +0.9 % over 128, 256 -1.5 %)
 constexpr int kMaxB = 20;       // multi-indices |b| <= 3
 
 template <int MM>

@@ -107,7 +107,7 @@ def test_parity_3d_generic(m, boundary):
 @pytest.mark.parametrize("m", [1, 2, 3])
 @pytest.mark.parametrize("boundary", [[0, 0, 0], [1, 1, 1], [1, 0, 0], [0, 1, 1]])
 def test_parity_3d_tiled_kernel(m, boundary):
-    # K crosses a partial 32-cell x tile and two 128-layer z chunks
+    # K crosses a partial 32-cell x tile and three 64-layer z chunks
     g, o = make_pair(3, m, [36, 2, 133], boundary=boundary, seed=40 + m)
     assert g.kernel_variant == 1
     run_both(g, o, 3, 0.25 * g.grid.h)
