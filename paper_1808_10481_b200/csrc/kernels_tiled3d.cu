@@ -211,6 +211,7 @@ __device__ __forceinline__ void ck(int c, int w, const TParams& P, const double 
                                    double (&acc)[(MM + 2) / 2][(MM + 2) / 2][(MM + 2) / 2]) {
   if constexpr (MM == 1) m1_ck(c, w, P, pt, acc);
   else if constexpr (MM == 2) m2_ck(c, w, P, pt, acc);
+  else if (c < 0) m3_ck_1(P, pt, acc);  // merged pressure launch: no index shift (the shared shift-0 body)
   else m3_ck(c, w, P, pt, acc);
 }
 
@@ -385,10 +386,17 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     __syncthreads();
   };
   // class of this warp in the Z + CK stage
-#ifndef HLF_NO_V7
+  // V7: the two q_z parities of a class share a warp (lane halves).  With TMA
+  // loads it still wins for the pressure launches (V_z launch 45.8 vs 47.6 ms)
+  // but the velocity launch, with three CK bodies and the z-shift selects of
+  // its z component, is faster in the plain one-class-per-warp layout
+  // (62.2 vs 68.8 ms at 512x512x256).  HLF_NO_V7 / HLF_V7 force one layout.
+#if defined(HLF_NO_V7)
+  constexpr bool V7 = false;
+#elif defined(HLF_V7)
   constexpr bool V7 = MM == 3;
 #else
-  constexpr bool V7 = false;
+  constexpr bool V7 = MM == 3 && NT != 3;
 #endif
   // V7 (m = 3): warp = (PX, PY, cell half), lane = (cell, PZ = lane >> 4)
   const int PX = (warp >> 2) & 1, PY = (warp >> 1) & 1;
