@@ -67,10 +67,6 @@ bool tiled2d_supported(int m);
 int launch_fill(const FillParams& p, cudaStream_t st);
 // field - amp prod sin_jet -> err[0] += sum of squared value errors, err[1] = max |jet error|
 int launch_error(const FillParams& p, cudaStream_t st);
-namespace v5 {
-// 16-warp tiled kernel, m = 3 (kernels_tiled3d_v5.cu)
-int launch(HalfKind kind, const HalfParams& p, cudaStream_t st);
-}
 // z ghost mirror for the dual family: dst layer = sign * (-1)^{c_z} src layer
 int launch_mirror_layer(double* dst, const double* src, int64_t plane, int n1, int d, double sigma,
                         cudaStream_t st);

@@ -709,10 +709,6 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
 bool tiled3d_supported(int m) { return m >= 1 && m <= 3; }
 
 int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st) {
-  // HLF_TILED_V5=1 selects the experimental 16-warp variant for m = 3 (A/B switch;
-  // it measured slower: shared-memory instruction queue bound)
-  static const bool use_v5 = std::getenv("HLF_TILED_V5") != nullptr;
-  if (m == 3 && use_v5) return v5::launch(kind, p, st);
   switch (m) {
     case 1: return launch_m<1>(kind, p, st);
     case 2: return launch_m<2>(kind, p, st);

@@ -261,111 +261,6 @@ def main():
 
 
 
-# ====================================================================== v5
-# 16 warps per CTA (<= 128 registers/thread), 32 cells, m = 3 only.
-#  XY: task = (l_z, q_x parity, cell half); lane = (cell in half, source row hi);
-#      half x-lines of the own row, row swap with lane ^ 16, y half-lines of
-#      q_y parity hi (per-lane coefficients cy absorb the row swap).
-#  Z+CK: warp = (parity class, column half h): P~ for the 8 columns with
-#      class-local i_x in {2h, 2h+1}; partial CK over those columns; the two
-#      halves of a class are summed through the target staging buffer.
-V5_TXC = 32
-V5_RAWX = 33
-
-
-def v5_gen_xy(mm, px):
-    n1, n = mm + 1, 2 * mm + 2
-    nh = n // 2
-    L = [f"__device__ __forceinline__ void v5_m{mm}_xy_px{px}(const TParams& P, const double* __restrict__ rb, double* __restrict__ wb,",
-         f"    const double (&cy)[{nh}][{n1}], double g) {{",
-         "  // rb = raw + (l_z*2 + hi)*RAWX + cell;  wb = ring_new + (hi*n1 + l_z)*TXC + cell"]
-    qxs = [q for q in range(n) if q % 2 == px]
-    for ly in range(n1):
-        def off(lx, side, ly=ly):
-            return f"rb[{(lx * n1 * n1 + ly * n1) * 2 * V5_RAWX + side}]"
-        res = half_line(mm, lambda l: off(l, 0), lambda l: off(l, 1), qxs, f"x{ly}", L)
-        for i, q in enumerate(qxs):
-            L.append(f"  const double xo{ly}_{i} = {res[q]};")
-            L.append(f"  const double xp{ly}_{i} = __shfl_xor_sync(0xffffffffu, xo{ly}_{i}, 16);")
-    for i, qx in enumerate(qxs):
-        for ly in range(n1):
-            sg = "g" if ly % 2 == 0 else "-g"
-            L.append(f"  const double u{i}_{ly} = fma({sg}, xp{ly}_{i}, xo{ly}_{i});")
-        for k in range(nh):
-            expr = "0.0"
-            for ly in range(n1):
-                expr = f"fma(cy[{k}][{ly}], u{i}_{ly}, {expr})"
-            L.append(f"  wb[{((qx * n + 2 * k) * n1) * V5_TXC}] = {expr};")
-    L.append("}")
-    return "\n".join(L)
-
-
-def v5_gen_z(mm, pz, h):
-    n1, n = mm + 1, 2 * mm + 2
-    nh = n // 2
-    L = [f"__device__ __forceinline__ void v5_m{mm}_z_pz{pz}_h{h}(const TParams& P, const double* __restrict__ ro,",
-         f"    const double* __restrict__ rn, double (&pt)[2][{nh}][{nh}]) {{",
-         "  // ro/rn = ring + ((PX*n + PY)*n1)*TXC + lane"]
-    for ixl in range(2):
-        ix = 2 * h + ixl
-        for iy in range(nh):
-            base = ((2 * ix) * n + 2 * iy) * n1
-            L.append("  {")
-            sub = []
-            res = half_line(mm, lambda l, base=base: f"ro[{(base + l) * V5_TXC}]",
-                            lambda l, base=base: f"rn[{(base + l) * V5_TXC}]",
-                            [pz + 2 * iz for iz in range(nh)], "z", sub)
-            L.extend("  " + t for t in sub)
-            for iz in range(nh):
-                L.append(f"    pt[{ixl}][{iy}][{iz}] = {res[pz + 2 * iz]};")
-            L.append("  }")
-    L.append("}")
-    return "\n".join(L)
-
-
-def v5_gen_ck(mm, c, sh, h):
-    """partial CK of component c (class-local shift sh along c) over the
-    columns with i_x in {2h, 2h+1}: acc[j] += GM[b] pt[j + b + sh e_c]."""
-    n1, n = mm + 1, 2 * mm + 2
-    nh, jh = n // 2, (n1 + 1) // 2
-    e = [int(c == a) for a in range(3)]
-    L = [f"__device__ __forceinline__ void v5_m{mm}_ck_c{c}_s{sh}_h{h}(const TParams& P, const double (&pt)[2][{nh}][{nh}],",
-         f"    double (&acc)[{jh}][{jh}][{jh}]) {{"]
-    for jx in range(jh):
-        for jy in range(jh):
-            for jz in range(jh):
-                j = (jx, jy, jz)
-                for b0 in range(mm + 1):
-                    for b1 in range(mm + 1 - b0):
-                        for b2 in range(mm + 1 - b0 - b1):
-                            b = (b0, b1, b2)
-                            i = [j[a] + b[a] + sh * e[a] for a in range(3)]
-                            if any(x >= nh for x in i) or i[0] // 2 != h:
-                                continue
-                            L.append(f"  acc[{jx}][{jy}][{jz}] = fma(P.GM[{bindex(b, mm)}], pt[{i[0] - 2 * h}][{i[1]}][{i[2]}], acc[{jx}][{jy}][{jz}]);")
-    L.append("}")
-    return "\n".join(L)
-
-
-def main_v5():
-    out = os.path.join(HERE, "..", "paper_1808_10481_b200", "csrc", "tiled3d_v5_gen.cuh")
-    mm = 3
-    parts = ["// GENERATED by tools/gen_tiled3d.py (v5) -- do not edit.",
-             "// 16-warp tiled 3D kernel stage code, m = 3 (kernels_tiled3d_v5.cu).", "#pragma once", ""]
-    for px in range(2):
-        parts += [v5_gen_xy(mm, px), ""]
-    for pz in range(2):
-        for h in range(2):
-            parts += [v5_gen_z(mm, pz, h), ""]
-    for c in range(3):
-        for sh in range(2):
-            for h in range(2):
-                parts += [v5_gen_ck(mm, c, sh, h), ""]
-    with open(out, "w") as f:
-        f.write("\n".join(parts))
-    print("wrote", out)
-
-
 # ====================================================================== v7
 # Z + CK stage with the two q_z-parity classes in one warp (m = 3):
 #   warp = (PX, PY, cell half), lane = (cell in half, PZ = lane >> 4).
@@ -435,5 +330,4 @@ def main_v7():
 
 if __name__ == "__main__":
     main()
-    main_v5()
     main_v7()
