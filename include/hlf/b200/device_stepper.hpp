@@ -36,6 +36,7 @@ class DeviceStepper {
     s_ = s;
     F_ = hlf_num_coeffs(s_);
     dim_ = desc.dim;
+    scheme_ = desc.scheme;
   }
   ~DeviceStepper() { hlf_destroy(s_); }
   DeviceStepper(const DeviceStepper&) = delete;
@@ -44,7 +45,11 @@ class DeviceStepper {
   int coeffs() const { return F_; }
   int dim() const { return dim_; }
   int64_t nodes(int grid) const { return hlf_num_nodes(s_, grid); }
-  int64_t field_nodes(int f) const { return nodes(f == 0 ? HLF_PRIMARY : HLF_DUAL); }
+  // leapfrog: p primary, v dual; the alternative 1D schemes: even fields primary, odd dual
+  int64_t field_nodes(int f) const {
+    const bool primary = scheme_ == HLF_SCHEME_LEAPFROG ? f == 0 : f % 2 == 0;
+    return nodes(primary ? HLF_PRIMARY : HLF_DUAL);
+  }
 
   void set_field(int f, const std::vector<double>& aos) {
     if (static_cast<int64_t>(aos.size()) != field_nodes(f) * F_)
@@ -71,7 +76,7 @@ class DeviceStepper {
 
  private:
   hlf_solver* s_ = nullptr;
-  int F_ = 0, dim_ = 0;
+  int F_ = 0, dim_ = 0, scheme_ = HLF_SCHEME_LEAPFROG;
 };
 
 }  // namespace hlf::b200

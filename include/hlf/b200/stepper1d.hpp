@@ -14,12 +14,15 @@
 // run on the device and download them.  advance_n (an extension) keeps the
 // state on the device for n steps and is the call to use for long runs.
 //
-// Coverage: the Hermite-leapfrog variant (step_system).  Coefficient jets are
-// taken from the problem at construction like the reference (stepper1d.cpp:
-// 103-110): constant ap/av run the constant-coefficient kernels, a varying ap
-// runs the per-node ap-jet kernels (av must be constant).  Problems with a
-// forcing provider, a varying av, or the modified / Dual-Hermite variants are
-// rejected with ConfigError (the reference's CPU Stepper1d still covers them).
+// Coverage: the Hermite-leapfrog variant (step_system) and, for constant
+// coefficients, the modified (init_modified / step_modified) and classic
+// Dual-Hermite (init_dual_hermite / step_dual_hermite) variants, bit-identical
+// to the reference.  Coefficient jets are taken from the problem at
+// construction like the reference (stepper1d.cpp:103-110): constant ap/av run
+// the constant-coefficient kernels, a varying ap runs the per-node ap-jet
+// kernels (leapfrog only; av must be constant).  Problems with a forcing
+// provider or a varying av are rejected with ConfigError (the reference's CPU
+// Stepper1d still covers them).
 #pragma once
 
 #include <cstring>
@@ -81,6 +84,8 @@ class Stepper1d {
       dev_->set_coeff(HLF_PRIMARY, ap_prim);
       dev_->set_coeff(HLF_DUAL, ap_dual);
     }
+    desc_ = d;
+    ap_const_ = ap_const;
   }
 
   // stepper1d.cpp:131-145
@@ -121,6 +126,67 @@ class Stepper1d {
     download(st);
   }
 
+  // ---- modified Hermite-leapfrog (stepper1d.cpp:174-232)
+  ModifiedState1d init_modified(double dt, double t0 = 0.0) const {
+    ModifiedState1d st;
+    st.dt = dt;
+    st.t = t0;
+    st.prim.resize(prob_.n_fields);
+    st.dual.resize(prob_.n_fields);
+    for (int f = 0; f < prob_.n_fields; ++f) {
+      st.prim[f].resize(grid_.K);
+      st.dual[f].resize(grid_.K);
+      for (int j = 0; j < grid_.K; ++j) {
+        st.prim[f][j] = prob_.exact(f, grid_.primary(j), t0, grid_.h, m_ + 1);
+        st.dual[f][j] = prob_.exact(f, grid_.dual(j), t0 + dt / 2.0, grid_.h, m_ + 1);
+      }
+    }
+    return st;
+  }
+  void step_modified(ModifiedState1d& st, int step_index) const {
+    DeviceStepper& dev = alt(HLF_SCHEME_MODIFIED);
+    // device fields: 0 = p primary, 1 = v dual, 2 = v primary, 3 = p dual
+    const std::vector<Jet>* in[4] = {&st.prim[0], &st.dual[1], &st.prim[1], &st.dual[0]};
+    for (int f = 0; f < 4; ++f) dev.set_field(f, flat(*in[f]));
+    dev.set_times(st.t, st.t + st.dt / 2.0, st.dt);
+    auto down = [&] {
+      std::vector<Jet>* out[4] = {&st.prim[0], &st.dual[1], &st.prim[1], &st.dual[0]};
+      for (int f = 0; f < 4; ++f) unflat(dev.get_field(f), *out[f]);
+      double tv = 0.0, dt = 0.0;
+      dev.times(st.t, tv, dt);
+    };
+    alt_guarded([&] { dev.step(step_index); }, down);
+    down();
+  }
+
+  // ---- classic two-half-step Hermite baseline (stepper1d.cpp:235-272)
+  DualState1d init_dual_hermite(double dt, double t0 = 0.0) const {
+    DualState1d st;
+    st.dt = dt;
+    st.t = t0;
+    st.p.resize(grid_.K);
+    st.v.resize(grid_.K);
+    for (int j = 0; j < grid_.K; ++j) {
+      st.p[j] = prob_.exact(0, grid_.primary(j), t0, grid_.h, m_ + 1);
+      st.v[j] = prob_.exact(1, grid_.primary(j), t0, grid_.h, m_ + 1);
+    }
+    return st;
+  }
+  void step_dual_hermite(DualState1d& st, int step_index) const {
+    DeviceStepper& dev = alt(HLF_SCHEME_DUAL_HERMITE);
+    dev.set_field(0, flat(st.p));
+    dev.set_field(2, flat(st.v));
+    dev.set_times(st.t, st.t, st.dt);
+    auto down = [&] {
+      unflat(dev.get_field(0), st.p);
+      unflat(dev.get_field(2), st.v);
+      double tv = 0.0, dt = 0.0;
+      dev.times(st.t, tv, dt);
+    };
+    alt_guarded([&] { dev.step(step_index); }, down);
+    down();
+  }
+
   const Problem1d& problem() const { return prob_; }
   const Grid1d& grid() const { return grid_; }
   const InterpOperator& op() const { return op_; }
@@ -132,6 +198,53 @@ class Stepper1d {
   int m_, n_;
   InterpOperator op_;
   std::unique_ptr<DeviceStepper> dev_;
+  hlf_desc desc_{};
+  bool ap_const_ = true;
+  mutable std::unique_ptr<DeviceStepper> alt_dev_[3];  // per alternative scheme, created on first use
+
+  DeviceStepper& alt(int scheme) const {
+    if (!ap_const_) throw ConfigError("the modified / Dual-Hermite device path needs constant coefficients");
+    if (!alt_dev_[scheme]) {
+      hlf_desc d = desc_;
+      d.scheme = scheme;
+      d.variable_ap = 0;
+      try {
+        alt_dev_[scheme] = std::make_unique<DeviceStepper>(d);
+      } catch (const Error& e) {
+        if (e.status == HLF_CONFIG_ERROR) throw ConfigError(e.what());
+        throw;
+      }
+    }
+    return *alt_dev_[scheme];
+  }
+  std::vector<double> flat(const std::vector<Jet>& jets) const {
+    const int n1 = m_ + 1;
+    if (static_cast<int>(jets.size()) != grid_.K) throw std::invalid_argument("one jet per node expected");
+    std::vector<double> out(static_cast<size_t>(grid_.K) * n1);
+    for (int j = 0; j < grid_.K; ++j) {
+      if (static_cast<int>(jets[j].size()) != n1) throw std::invalid_argument("jets must hold m+1 entries");
+      std::memcpy(out.data() + static_cast<size_t>(j) * n1, jets[j].data(), sizeof(double) * n1);
+    }
+    return out;
+  }
+  void unflat(const std::vector<double>& in, std::vector<Jet>& jets) const {
+    const int n1 = m_ + 1;
+    for (int j = 0; j < grid_.K; ++j)
+      std::memcpy(jets[j].data(), in.data() + static_cast<size_t>(j) * n1, sizeof(double) * n1);
+  }
+  template <class Fn, class Down>
+  void alt_guarded(Fn&& fn, Down&& down) const {
+    try {
+      fn();
+    } catch (const Error& e) {
+      if (e.status == HLF_INSTABILITY) {
+        down();
+        throw InstabilityError(instability_step(e.what()), e.what());
+      }
+      if (e.status == HLF_CONFIG_ERROR) throw ConfigError(e.what());
+      throw;
+    }
+  }
 
   void upload(const State1d& st) const {
     const int n1 = m_ + 1;

@@ -69,7 +69,24 @@ typedef struct hlf_desc {
   void* stream;       /* cudaStream_t to launch on; NULL = the library's own stream */
   int z_slab;         /* 1: z is one slab of a periodic decomposition; z halos come
                          from hlf_halo_* instead of the local wrap */
+  int scheme;         /* HLF_SCHEME_*: the reference Stepper1d's three time schemes
+                         (config.hpp:9); the alternatives are 1D, periodic, constant
+                         coefficients */
 } hlf_desc;
+
+/* time schemes (hlf::Variant, config.hpp:9):
+   LEAPFROG     staggered Hermite-leapfrog (advance_p / advance_v / step_system,
+                stepper1d.cpp:147-172): field 0 = p on the primary grid, 1..d = v on the dual grid;
+   MODIFIED     step_modified (stepper1d.cpp:191-232): every field on both grids:
+                field 0 = p primary (t), 1 = v dual (t + dt/2), 2 = v primary (t), 3 = p dual (t + dt/2);
+   DUAL_HERMITE step_dual_hermite (stepper1d.cpp:249-272), both fields co-located:
+                field 0 = p primary, 2 = v primary (t); fields 1, 3 are the midpoint scratch
+                on the dual grid.
+   hlf_step / hlf_advance_n run the selected scheme; the time stamp t is t_p
+   (hlf_get_times), t_v = t_p + dt/2 (MODIFIED) or t_p (DUAL_HERMITE). */
+#define HLF_SCHEME_LEAPFROG 0
+#define HLF_SCHEME_MODIFIED 1
+#define HLF_SCHEME_DUAL_HERMITE 2
 
 /* --- interpolation operator ---------------------------------------------- */
 /* M = A^{-1} (row-major, (2m+2)^2) and its 1-norm condition; HLF_CONFIG_ERROR for m outside [0, 8] */

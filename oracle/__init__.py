@@ -80,6 +80,13 @@ def ref_lib():
         L.ref1d_coeff.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp]
         L.ref1d_has_forcing.argtypes = [C.c_void_p]
         L.ref1d_has_forcing.restype = C.c_int
+        for f in ("ref1d_init_modified", "ref1d_init_dual"):
+            getattr(L, f).argtypes = [C.c_void_p, C.c_double, C.c_double]
+        L.ref1d_get_modified.argtypes = [C.c_void_p] + [_dp] * 5
+        L.ref1d_get_dual.argtypes = [C.c_void_p] + [_dp] * 3
+        for f in ("ref1d_steps_modified", "ref1d_steps_dual"):
+            getattr(L, f).argtypes = [C.c_void_p, C.c_int, C.c_int]
+            getattr(L, f).restype = C.c_int
         L.ref2d_exact.argtypes = [C.c_char_p, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, _dp]
         L.ref2d_exact.restype = C.c_int
         L.ref2d_l2_acoustics.argtypes = [C.c_int, C.c_int, C.c_double] + [_dp] * 6 + [C.c_int, _dp, C.c_int, C.c_double]
@@ -219,6 +226,34 @@ class RefStepper1d:
 
     def has_forcing(self) -> bool:
         return bool(self.L.ref1d_has_forcing(self.h_))
+
+    # the reference's alternative time schemes (stepper1d.cpp:174-272)
+    def init_modified(self, dt: float, t0: float = 0.0):
+        self.L.ref1d_init_modified(self.h_, dt, t0)
+
+    def get_modified(self):
+        """(p primary, v primary, p dual, v dual) as [K, m+1] arrays, and (t, dt)"""
+        n1 = self.m + 1
+        arrs = [np.zeros(self.K * n1) for _ in range(4)]
+        tdt = np.zeros(2)
+        self.L.ref1d_get_modified(self.h_, *[_ptr(a) for a in arrs], _ptr(tdt))
+        return [a.reshape(self.K, n1) for a in arrs], tuple(tdt)
+
+    def steps_modified(self, n: int, first: int = 0) -> int:
+        return self.L.ref1d_steps_modified(self.h_, n, first)
+
+    def init_dual(self, dt: float, t0: float = 0.0):
+        self.L.ref1d_init_dual(self.h_, dt, t0)
+
+    def get_dual(self):
+        """(p, v) on the primary grid as [K, m+1] arrays, and (t, dt)"""
+        n1 = self.m + 1
+        p, v, tdt = np.zeros(self.K * n1), np.zeros(self.K * n1), np.zeros(2)
+        self.L.ref1d_get_dual(self.h_, _ptr(p), _ptr(v), _ptr(tdt))
+        return (p.reshape(self.K, n1), v.reshape(self.K, n1)), tuple(tdt)
+
+    def steps_dual(self, n: int, first: int = 0) -> int:
+        return self.L.ref1d_steps_dual(self.h_, n, first)
 
 
 def ref_dt_nominal(dim: int, cfl: float, h: float, c_max: float) -> float:

@@ -50,6 +50,8 @@ bool make_problem(const char* name, unsigned seed, Problem1d& out) {
 struct Ref1d {
   std::unique_ptr<Stepper1d> stepper;
   State1d st;
+  ModifiedState1d mst;  // step_modified state (stepper1d.cpp:174-232)
+  DualState1d dst;      // step_dual_hermite state (stepper1d.cpp:235-272)
 };
 
 }  // namespace
@@ -259,5 +261,57 @@ double ref_dt_nominal(int dim, double cfl, double h, double c_max) {
 }
 
 int ref_step_count(double T, double dt) { return step_count(T, dt); }
+
+// ---- the reference's alternative time schemes: jets flat [node][coef]
+void ref1d_init_modified(void* h, double dt, double t0) {
+  Ref1d* r = static_cast<Ref1d*>(h);
+  r->mst = r->stepper->init_modified(dt, t0);
+}
+// fields in the order p primary, v primary, p dual, v dual; tdt = {t, dt}
+void ref1d_get_modified(void* h, double* pp, double* vp, double* pd, double* vd, double* tdt) {
+  const ModifiedState1d& st = static_cast<Ref1d*>(h)->mst;
+  double* outs[4] = {pp, vp, pd, vd};
+  const std::vector<Jet>* ins[4] = {&st.prim[0], &st.prim[1], &st.dual[0], &st.dual[1]};
+  for (int f = 0; f < 4; ++f) {
+    size_t k = 0;
+    for (const Jet& j : *ins[f])
+      for (double x : j) outs[f][k++] = x;
+  }
+  tdt[0] = st.t;
+  tdt[1] = st.dt;
+}
+int ref1d_steps_modified(void* h, int n, int first) {
+  Ref1d* r = static_cast<Ref1d*>(h);
+  try {
+    for (int i = 0; i < n; ++i) r->stepper->step_modified(r->mst, first + i);
+  } catch (const InstabilityError& e) {
+    return e.step;
+  }
+  return -1;
+}
+void ref1d_init_dual(void* h, double dt, double t0) {
+  Ref1d* r = static_cast<Ref1d*>(h);
+  r->dst = r->stepper->init_dual_hermite(dt, t0);
+}
+void ref1d_get_dual(void* h, double* p, double* v, double* tdt) {
+  const DualState1d& st = static_cast<Ref1d*>(h)->dst;
+  size_t k = 0;
+  for (const Jet& j : st.p)
+    for (double x : j) p[k++] = x;
+  k = 0;
+  for (const Jet& j : st.v)
+    for (double x : j) v[k++] = x;
+  tdt[0] = st.t;
+  tdt[1] = st.dt;
+}
+int ref1d_steps_dual(void* h, int n, int first) {
+  Ref1d* r = static_cast<Ref1d*>(h);
+  try {
+    for (int i = 0; i < n; ++i) r->stepper->step_dual_hermite(r->dst, first + i);
+  } catch (const InstabilityError& e) {
+    return e.step;
+  }
+  return -1;
+}
 
 }  // extern "C"

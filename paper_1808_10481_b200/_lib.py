@@ -43,6 +43,7 @@ class HlfDesc(C.Structure):
         ("device", C.c_int),
         ("stream", C.c_void_p),
         ("z_slab", C.c_int),
+        ("scheme", C.c_int),
     ]
 
 

@@ -28,6 +28,8 @@ struct hlf_solver {
   double h = 1.0, ap = -1.0, av = -1.0;
   bool variable = false;
   bool z_slab = false;
+  int scheme = HLF_SCHEME_LEAPFROG;
+  int nfields = 2;              // d + 1, or 4 for the 1D alternative schemes
   double t_p = 0.0, t_v = 0.0, dt = 0.0;
   std::vector<double> M;
   int device = 0;
@@ -50,8 +52,11 @@ struct hlf_solver {
 
   int64_t layer_stride(int f) const { return plane[f] * F; }
   int zoff(int f) const { return (d == 3 && f > 0) ? 1 : 0; }
-  int grid_of(int f) const { return f == 0 ? HLF_PRIMARY : HLF_DUAL; }
-  const int* nodes_of(int f) const { return f == 0 ? Np : Nd; }
+  // leapfrog: p primary, v dual; alternative schemes: even fields primary, odd dual
+  int grid_of(int f) const {
+    return (scheme == HLF_SCHEME_LEAPFROG ? f == 0 : f % 2 == 0) ? HLF_PRIMARY : HLF_DUAL;
+  }
+  const int* nodes_of(int f) const { return grid_of(f) == HLF_PRIMARY ? Np : Nd; }
   int64_t num_nodes(int grid) const {
     const int* N = grid == HLF_PRIMARY ? Np : Nd;
     return static_cast<int64_t>(N[0]) * N[1] * N[2];
@@ -143,7 +148,7 @@ int ipow(int b, int e) {
   return r;
 }
 
-bool valid_field(const hlf_solver* s, int f) { return f >= 0 && f <= s->d; }
+bool valid_field(const hlf_solver* s, int f) { return f >= 0 && f < s->nfields; }
 
 hlf_status ensure_staging(hlf_solver* s, size_t bytes) {
   if (s->staging_bytes >= bytes) return HLF_OK;
@@ -241,6 +246,8 @@ void fill_weights(const hlf_solver* s, hlfk::HalfKind kind, HalfParams& P) {
 // the full launch with both field bases shifted by zlo layers, so every kernel
 // runs it unchanged.
 hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0, int zhi = -1) {
+  if (s->scheme != HLF_SCHEME_LEAPFROG)
+    return fail(s, HLF_CONFIG_ERROR, "half steps belong to the leapfrog scheme; use hlf_step");
   hlf_status st = fill_ghosts(s, kind == hlfk::PRE);
   if (st != HLF_OK) return st;
   HalfParams P;
@@ -340,6 +347,12 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
   }
   if (desc->z_slab && (d != 3 || desc->boundary[2] != HLF_PERIODIC))
     return fail(nullptr, HLF_CONFIG_ERROR, "z slabs need d = 3 with a periodic z axis");
+  if (desc->scheme < HLF_SCHEME_LEAPFROG || desc->scheme > HLF_SCHEME_DUAL_HERMITE)
+    return fail(nullptr, HLF_CONFIG_ERROR, "unknown time scheme");
+  if (desc->scheme != HLF_SCHEME_LEAPFROG &&
+      (d != 1 || desc->boundary[0] != HLF_PERIODIC || desc->variable_ap || desc->z_slab))
+    return fail(nullptr, HLF_CONFIG_ERROR,
+                "the modified and dual-Hermite schemes run in 1D, periodic, with constant coefficients");
 
   hlf_solver* s = new hlf_solver;
   s->d = d;
@@ -353,6 +366,8 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
   s->av = desc->av;
   s->variable = desc->variable_ap != 0;
   s->z_slab = desc->z_slab != 0;
+  s->scheme = desc->scheme;
+  s->nfields = desc->scheme == HLF_SCHEME_LEAPFROG ? d + 1 : 4;
   s->device = desc->device;
   for (int ax = 0; ax < 3; ++ax) {
     const bool used = ax < d;
@@ -381,7 +396,7 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
     if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaStreamCreate"));
     s->own_stream = true;
   }
-  for (int f = 0; f <= d; ++f) {
+  for (int f = 0; f < s->nfields; ++f) {
     const int* N = s->nodes_of(f);
     s->plane[f] = static_cast<int64_t>(N[0]) * N[1];
     // d = 3: p gets one upper ghost/halo layer unless the z walls already
@@ -537,7 +552,54 @@ hlf_status hlf_commit_half(hlf_solver* s, int half) {
   return HLF_OK;
 }
 
+// one step of the 1D modified / dual-Hermite scheme (stepper1d.cpp:191-272)
+static hlf_status scheme1d_step(hlf_solver* s, int step_index) {
+  hlfk::Scheme1dParams P;
+  std::memset(&P, 0, sizeof(P));
+  std::memcpy(P.M, s->M.data(), sizeof(double) * s->M.size());
+  P.h = s->h;
+  P.ap = s->ap;
+  P.av = s->av;
+  P.dt = s->dt;
+  P.K = s->K[0];
+  P.step = step_index;
+  P.flag = s->flag;
+  int launched = 0;
+  if (s->scheme == HLF_SCHEME_MODIFIED) {
+    // primary update from the dual copies, then dual update from the new primary
+    P.to_primary = 1;
+    P.src_p = s->field[3];
+    P.src_v = s->field[1];
+    P.dst_p = s->field[0];
+    P.dst_v = s->field[2];
+    launched += hlfk::launch_modified_1d(s->m, P, s->stream);
+    P.to_primary = 0;
+    P.src_p = s->field[0];
+    P.src_v = s->field[2];
+    P.dst_p = s->field[3];
+    P.dst_v = s->field[1];
+    launched += hlfk::launch_modified_1d(s->m, P, s->stream);
+  } else {
+    P.src_p = s->field[0];
+    P.src_v = s->field[2];
+    P.dst_p = s->field[1];
+    P.dst_v = s->field[3];
+    launched += hlfk::launch_dual_hermite_1d(s->m, 0, P, s->stream);
+    P.src_p = s->field[1];
+    P.src_v = s->field[3];
+    P.dst_p = s->field[0];
+    P.dst_v = s->field[2];
+    launched += hlfk::launch_dual_hermite_1d(s->m, 1, P, s->stream);
+  }
+  s->launches += launched;
+  HLF_CUDA(s, cudaGetLastError());
+  s->t_p += s->dt;
+  s->t_v = s->scheme == HLF_SCHEME_MODIFIED ? s->t_p + s->dt / 2.0 : s->t_p;
+  return HLF_OK;
+}
+
 static hlf_status step_async(hlf_solver* s, int step_index) {
+  if (s->scheme != HLF_SCHEME_LEAPFROG) return scheme1d_step(s, step_index);
   if (s->variable && (!s->coeff[0] || !s->coeff[1])) return fail(s, HLF_CONFIG_ERROR, "ap jets not set");
   hlf_status st = launch_half(s, hlfk::PRE, step_index);
   if (st != HLF_OK) return st;

@@ -57,7 +57,27 @@ struct FillParams {
   double* err;                  // launch_error: [sum of squared value errors, max |jet error|]
 };
 
+// 1D alternative schemes of the reference Stepper1d (periodic, constant
+// ap / av): the modified Hermite-leapfrog half pass (step_modified,
+// stepper1d.cpp:191-232) and the two passes of the classic two-half-step
+// Hermite scheme (step_dual_hermite, stepper1d.cpp:249-272).
+struct Scheme1dParams {
+  double M[kMaxN * kMaxN];
+  double h, ap, av, dt;
+  int K;                        // nodes per grid (periodic)
+  int to_primary;               // modified: 1 = dual -> primary half, 0 = primary -> dual
+  const double* src_p;          // the two fields of the source grid [coef][node]
+  const double* src_v;
+  double* dst_p;                // targets (modified: updated in place from their previous value)
+  double* dst_v;
+  int step;
+  int* flag;
+};
+
 // launchers (return the number of kernels launched)
+int launch_modified_1d(int m, const Scheme1dParams& p, cudaStream_t st);
+// pass 0: dual midpoints from the primary grid; pass 1: primary from the midpoints
+int launch_dual_hermite_1d(int m, int pass, const Scheme1dParams& p, cudaStream_t st);
 int launch_half_generic(int d, int m, bool variable, HalfKind kind, const HalfParams& p,
                         cudaStream_t st);
 int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);

@@ -400,7 +400,167 @@ int launch_dm(bool variable, HalfKind kind, const HalfParams& p, cudaStream_t st
   return 1;
 }
 
+// ---- 1D alternative schemes (faithful arithmetic, reference operation order)
+
+// both CK tables of ck_recurrence_variable (stepper1d.cpp:22-38) level by
+// level from the reconstructions of the two fields; `sink(r, Pr, Vr)` sees
+// every level r = 0..n-1 in order
+template <int MM, typename Sink>
+__device__ __forceinline__ void ck_tables_1d(const Scheme1dParams& P, const double (&Tp)[2 * MM + 2],
+                                             const double (&Tv)[2 * MM + 2], Sink sink) {
+  constexpr int n = 2 * MM + 2;
+  double Pc[n], Vc[n];
+#pragma unroll
+  for (int e = 0; e < n; ++e) {
+    Pc[e] = Tp[e];
+    Vc[e] = Tv[e];
+  }
+  sink(0, Pc, Vc);
+#pragma unroll
+  for (int r = 0; r + 1 < n; ++r) {
+    double Pn[n], Vn[n];
+#pragma unroll
+    for (int e = 0; e < n; ++e) {
+      // jet_multiply(ap, jet_differentiate(V, 1, h)) with ap = [ap, 0, ...]:
+      // out = 0.0 + ap * (V[e+1] * (e+1) / h)  (jet.cpp:8-31)
+      const double dv = e + 1 < n ? __ddiv_rn(__dmul_rn(Vc[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P.h) : 0.0;
+      const double dp = e + 1 < n ? __ddiv_rn(__dmul_rn(Pc[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P.h) : 0.0;
+      Pn[e] = __dadd_rn(0.0, __dmul_rn(P.ap, dv));
+      Vn[e] = __dadd_rn(0.0, __dmul_rn(P.av, dp));
+    }
+#pragma unroll
+    for (int e = 0; e < n; ++e) {
+      Pc[e] = Pn[e];
+      Vc[e] = Vn[e];
+    }
+    sink(r + 1, Pc, Vc);
+  }
+}
+
+// reconstruct_cell_1d + interp_apply (interpolation.cpp:53-75) for both fields
+template <int MM>
+__device__ __forceinline__ void reconstruct_pv_1d(const Scheme1dParams& P, int li, int ri, double (&Tp)[2 * MM + 2],
+                                                  double (&Tv)[2 * MM + 2]) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  double Sp[n], Sv[n];
+#pragma unroll
+  for (int a = 0; a < n1; ++a) {
+    Sp[a] = __ldg(P.src_p + li + a * P.K);
+    Sp[n1 + a] = __ldg(P.src_p + ri + a * P.K);
+    Sv[a] = __ldg(P.src_v + li + a * P.K);
+    Sv[n1 + a] = __ldg(P.src_v + ri + a * P.K);
+  }
+#pragma unroll
+  for (int r = 0; r < n; ++r) {
+    double ap_ = 0.0, av_ = 0.0;
+#pragma unroll
+    for (int s2 = 0; s2 < n; ++s2) {
+      ap_ = __dadd_rn(ap_, __dmul_rn(P.M[r * n + s2], Sp[s2]));
+      av_ = __dadd_rn(av_, __dmul_rn(P.M[r * n + s2], Sv[s2]));
+    }
+    Tp[r] = ap_;
+    Tv[r] = av_;
+  }
+}
+
+// one half of step_modified: out = modified_advance(prev, table) for p and v
+// (stepper1d.cpp:73-91, 191-232)
+template <int MM>
+__global__ void __launch_bounds__(128) modified_1d(const __grid_constant__ Scheme1dParams P) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  const int j = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= P.K) return;
+  const int li = P.to_primary ? (j == 0 ? P.K - 1 : j - 1) : j;
+  const int ri = P.to_primary ? j : (j + 1 == P.K ? 0 : j + 1);
+  double Tp[n], Tv[n];
+  reconstruct_pv_1d<MM>(P, li, ri, Tp, Tv);
+  double op[n1], ov[n1];
+#pragma unroll
+  for (int s2 = 0; s2 < n1; ++s2) {
+    const double pp = P.dst_p[j + s2 * P.K], pv = P.dst_v[j + s2 * P.K];
+    op[s2] = s2 % 2 == 0 ? pp : -pp;
+    ov[s2] = s2 % 2 == 0 ? pv : -pv;
+  }
+  double w = 2.0;  // w[0] = 2, w[r] = w[r-1] * dt / 2 / r
+  ck_tables_1d<MM>(P, Tp, Tv, [&](int r, const double (&Pr)[n], const double (&Vr)[n]) {
+    if (r > 0) w = __ddiv_rn(__ddiv_rn(__dmul_rn(w, P.dt), 2.0), static_cast<double>(r));
+#pragma unroll
+    for (int s2 = 0; s2 < n1; ++s2) {
+      if ((s2 % 2 == 0) == (r % 2 == 1)) {  // even s: odd levels; odd s: even levels
+        op[s2] = __dadd_rn(op[s2], __dmul_rn(w, Pr[s2]));
+        ov[s2] = __dadd_rn(ov[s2], __dmul_rn(w, Vr[s2]));
+      }
+    }
+  });
+  bool bad = false;
+#pragma unroll
+  for (int s2 = 0; s2 < n1; ++s2) {
+    bad |= !isfinite(op[s2]) || !isfinite(ov[s2]);
+    P.dst_p[j + s2 * P.K] = op[s2];
+    P.dst_v[j + s2 * P.K] = ov[s2];
+  }
+  if (bad && P.step >= 0) atomicMin(P.flag, P.step);
+}
+
+// one pass of step_dual_hermite: taylor_advance by tau = dt/2 (stepper1d.cpp:63-71, 249-272)
+template <int MM, int PASS>
+__global__ void __launch_bounds__(128) dual_hermite_1d(const __grid_constant__ Scheme1dParams P) {
+  constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  const int j = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= P.K) return;
+  const int li = PASS == 0 ? j : (j == 0 ? P.K - 1 : j - 1);
+  const int ri = PASS == 0 ? (j + 1 == P.K ? 0 : j + 1) : j;
+  double Tp[n], Tv[n];
+  reconstruct_pv_1d<MM>(P, li, ri, Tp, Tv);
+  const double tau = __ddiv_rn(P.dt, 2.0);
+  double op[n1], ov[n1];
+#pragma unroll
+  for (int s2 = 0; s2 < n1; ++s2) op[s2] = ov[s2] = 0.0;
+  double w = 1.0;
+  ck_tables_1d<MM>(P, Tp, Tv, [&](int r, const double (&Pr)[n], const double (&Vr)[n]) {
+    if (r > 0) w = __dmul_rn(w, __ddiv_rn(tau, static_cast<double>(r)));
+#pragma unroll
+    for (int s2 = 0; s2 < n1; ++s2) {
+      op[s2] = __dadd_rn(op[s2], __dmul_rn(w, Pr[s2]));
+      ov[s2] = __dadd_rn(ov[s2], __dmul_rn(w, Vr[s2]));
+    }
+  });
+  bool bad = false;
+#pragma unroll
+  for (int s2 = 0; s2 < n1; ++s2) {
+    bad |= !isfinite(op[s2]) || !isfinite(ov[s2]);
+    P.dst_p[j + s2 * P.K] = op[s2];
+    P.dst_v[j + s2 * P.K] = ov[s2];
+  }
+  if (PASS == 1 && bad && P.step >= 0) atomicMin(P.flag, P.step);
+}
+
 }  // namespace
+
+int launch_modified_1d(int m, const Scheme1dParams& p, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((p.K + 127) / 128);
+  switch (m) {
+#define HLF_M(MM) \
+  case MM: modified_1d<MM><<<blocks, 128, 0, st>>>(p); return 1;
+    HLF_M(0) HLF_M(1) HLF_M(2) HLF_M(3) HLF_M(4) HLF_M(5) HLF_M(6) HLF_M(7) HLF_M(8)
+#undef HLF_M
+    default: return -1;
+  }
+}
+
+int launch_dual_hermite_1d(int m, int pass, const Scheme1dParams& p, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((p.K + 127) / 128);
+  switch (m) {
+#define HLF_M(MM)                                                            \
+  case MM:                                                                   \
+    if (pass == 0) dual_hermite_1d<MM, 0><<<blocks, 128, 0, st>>>(p);        \
+    else dual_hermite_1d<MM, 1><<<blocks, 128, 0, st>>>(p);                  \
+    return 1;
+    HLF_M(0) HLF_M(1) HLF_M(2) HLF_M(3) HLF_M(4) HLF_M(5) HLF_M(6) HLF_M(7) HLF_M(8)
+#undef HLF_M
+    default: return -1;
+  }
+}
 
 int launch_half_generic(int d, int m, bool variable, HalfKind kind, const HalfParams& p,
                         cudaStream_t st) {

@@ -73,6 +73,10 @@ def step_count(T: float, dt_nominal: float) -> int:
     return int(math.ceil(T / dt_nominal))
 
 
+# time schemes (hlf::Variant, config.hpp:9; hlf_b200.h HLF_SCHEME_*)
+SCHEME_LEAPFROG, SCHEME_MODIFIED, SCHEME_DUAL_HERMITE = 0, 1, 2
+
+
 @dataclass
 class SchemeConfig:
     """hlf::SchemeConfig (config.hpp:30-44); dt_nominal_3d extends the 2D rule
@@ -185,7 +189,7 @@ class Stepper:
 
     def __init__(self, grid: Grid, m: int, boundary=None, ap: float = -1.0, av: float = -1.0,
                  variable_ap: bool = False, M: np.ndarray | None = None, device: int = 0,
-                 stream: int | None = None, z_slab: bool = False):
+                 stream: int | None = None, z_slab: bool = False, scheme: int = 0):
         SchemeConfig(m=m).validate()  # Stepper1d ctor guard (stepper1d.cpp:95-98)
         L = _L.lib()
         d = grid.dim
@@ -207,11 +211,13 @@ class Stepper:
         desc.device = device
         desc.stream = stream
         desc.z_slab = int(z_slab)
+        desc.scheme = int(scheme)
         h = C.c_void_p()
         _check(L.hlf_create(C.byref(desc), C.byref(h)), None)
         self._h = h
         self._L = L
         self.grid, self.m, self.dim = grid, m, d
+        self.scheme = int(scheme)
         self.boundary = boundary
         self.ap, self.av = ap, av
         self.n1, self.n = m + 1, 2 * m + 2
@@ -239,7 +245,9 @@ class Stepper:
         return int(self._L.hlf_num_nodes(self._h, grid))
 
     def field_nodes(self, f: int) -> int:
-        return self.num_nodes(PRIMARY if f == 0 else DUAL)
+        # leapfrog: p primary, v dual; modified / dual-Hermite: even fields primary
+        primary = f == 0 if self.scheme == SCHEME_LEAPFROG else f % 2 == 0
+        return self.num_nodes(PRIMARY if primary else DUAL)
 
     def node_shape(self, f: int) -> tuple:
         K = self.grid.K

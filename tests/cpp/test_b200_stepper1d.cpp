@@ -242,3 +242,33 @@ TEST_CASE("unsupported problem features are configuration errors") {
   Problem1d adv = advection_problem();
   CHECK_THROWS_AS(DeviceStepper1d(adv, g, 2), ConfigError);                       // one field
 }
+
+TEST_CASE("modified and Dual-Hermite variants match the reference bit for bit") {
+  // stepper1d.cpp:174-272 on the device (constant coefficients)
+  for (const Problem1d& prob : {standing_wave_problem(), random_wave_problem(1234)}) {
+    for (int m = 0; m <= 4; ++m) {
+      Grid1d g = Grid1d::over(prob.x_min, prob.x_max, 24);
+      Stepper1d ref(prob, g, m);
+      DeviceStepper1d dev(prob, g, m);
+      const double dt = 0.5 * g.h / prob.c_max;
+      ModifiedState1d a = ref.init_modified(dt), b = dev.init_modified(dt);
+      for (int i = 0; i < 25; ++i) {
+        ref.step_modified(a, i);
+        dev.step_modified(b, i);
+      }
+      for (int f = 0; f < 2; ++f) {
+        CHECK(max_rel(b.prim[f], a.prim[f]) == 0.0);
+        CHECK(max_rel(b.dual[f], a.dual[f]) == 0.0);
+      }
+      CHECK(b.t == a.t);
+      DualState1d c = ref.init_dual_hermite(dt), d = dev.init_dual_hermite(dt);
+      for (int i = 0; i < 25; ++i) {
+        ref.step_dual_hermite(c, i);
+        dev.step_dual_hermite(d, i);
+      }
+      CHECK(max_rel(d.p, c.p) == 0.0);
+      CHECK(max_rel(d.v, c.v) == 0.0);
+      CHECK(d.t == c.t);
+    }
+  }
+}
