@@ -238,6 +238,10 @@ void fill_weights(const hlf_solver* s, hlfk::HalfKind kind, HalfParams& P) {
   }
   P.inv_h = 1.0 / s->h;
   P.h = s->h;
+  {
+    int e2 = 0;
+    P.pow2_h = std::frexp(s->h, &e2) == 0.5;
+  }
   P.ap = s->ap;
   P.av = s->av;
 }
@@ -558,6 +562,11 @@ static hlf_status scheme1d_step(hlf_solver* s, int step_index) {
   std::memset(&P, 0, sizeof(P));
   std::memcpy(P.M, s->M.data(), sizeof(double) * s->M.size());
   P.h = s->h;
+  P.inv_h = 1.0 / s->h;
+  {
+    int e2 = 0;
+    P.pow2_h = std::frexp(s->h, &e2) == 0.5;
+  }
   P.ap = s->ap;
   P.av = s->av;
   P.dt = s->dt;

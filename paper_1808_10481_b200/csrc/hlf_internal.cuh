@@ -29,6 +29,7 @@ struct HalfParams {
   double G[kMaxM + 1];
   double w[kMaxN];              // w_r for the iterated (variable-coefficient) form
   double inv_h, h;
+  int pow2_h;                   // h is a power of two: x / h == x * inv_h exactly (faithful kernels)
   double ap, av;
   const double* src[3];         // source field bases (layer 0 of the allocation)
   double* dst[3];               // target field bases
@@ -64,6 +65,8 @@ struct FillParams {
 struct Scheme1dParams {
   double M[kMaxN * kMaxN];
   double h, ap, av, dt;
+  double inv_h;
+  int pow2_h;                   // h is a power of two: x / h == x * inv_h exactly
   int K;                        // nodes per grid (periodic)
   int to_primary;               // modified: 1 = dual -> primary half, 0 = primary -> dual
   const double* src_p;          // the two fields of the source grid [coef][node]

@@ -23,6 +23,14 @@ namespace {
 
 __host__ __device__ constexpr int cpow(int b, int e) { return e == 0 ? 1 : b * cpow(b, e - 1); }
 
+// x / h of jet_differentiate (jet.cpp:20-31).  When h is a power of two the
+// quotient equals x * (1/h) bit for bit (both are the correctly rounded value
+// of the same real number), so the faithful kernels skip the IEEE division.
+template <class Params>
+__device__ __forceinline__ double div_h(double x, const Params& P) {
+  return P.pow2_h ? __dmul_rn(x, P.inv_h) : __ddiv_rn(x, P.h);
+}
+
 template <int D>
 struct Idx {
   // tensor of extent N per axis, x-major: e = sum_ax q_ax N^(D-1-ax)
@@ -183,7 +191,7 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
           const int qc = (e / stride) % n;
-          const double dv = qc + 1 < n ? __ddiv_rn(__dmul_rn(Pt[e + stride], static_cast<double>(qc + 1)), P.h) : 0.0;
+          const double dv = qc + 1 < n ? div_h(__dmul_rn(Pt[e + stride], static_cast<double>(qc + 1)), P) : 0.0;
           Vt[c * E + e] = __dmul_rn(P.av, dv);
         }
       }
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
           const int qc = (e / stride) % n;
-          const double dv = qc + 1 < n ? __ddiv_rn(__dmul_rn(Vt[c * E + e + stride], static_cast<double>(qc + 1)), P.h) : 0.0;
+          const double dv = qc + 1 < n ? div_h(__dmul_rn(Vt[c * E + e + stride], static_cast<double>(qc + 1)), P) : 0.0;
           S[e] = __dadd_rn(S[e], dv);
         }
       }
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(128) half_1d(const __grid_constant__ HalfParam
     if (p_live) {
 #pragma unroll
       for (int e = 0; e < n; ++e) {
-        const double dv = e + 1 < n ? __ddiv_rn(__dmul_rn(Pt[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P.h)
+        const double dv = e + 1 < n ? div_h(__dmul_rn(Pt[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P)
                                     : 0.0;
         Vt[e] = __dmul_rn(P.av, dv);
       }
@@ -339,7 +347,7 @@ __global__ void __launch_bounds__(128) half_1d(const __grid_constant__ HalfParam
       double Sd[n];
 #pragma unroll
       for (int e = 0; e < n; ++e) {
-        const double dv = e + 1 < n ? __ddiv_rn(__dmul_rn(Vt[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P.h)
+        const double dv = e + 1 < n ? div_h(__dmul_rn(Vt[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P)
                                     : 0.0;
         Sd[e] = __dadd_rn(0.0, dv);
       }
@@ -423,8 +431,8 @@ __device__ __forceinline__ void ck_tables_1d(const Scheme1dParams& P, const doub
     for (int e = 0; e < n; ++e) {
       // jet_multiply(ap, jet_differentiate(V, 1, h)) with ap = [ap, 0, ...]:
       // out = 0.0 + ap * (V[e+1] * (e+1) / h)  (jet.cpp:8-31)
-      const double dv = e + 1 < n ? __ddiv_rn(__dmul_rn(Vc[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P.h) : 0.0;
-      const double dp = e + 1 < n ? __ddiv_rn(__dmul_rn(Pc[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P.h) : 0.0;
+      const double dv = e + 1 < n ? div_h(__dmul_rn(Vc[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P) : 0.0;
+      const double dp = e + 1 < n ? div_h(__dmul_rn(Pc[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P) : 0.0;
       Pn[e] = __dadd_rn(0.0, __dmul_rn(P.ap, dv));
       Vn[e] = __dadd_rn(0.0, __dmul_rn(P.av, dp));
     }
@@ -483,7 +491,7 @@ __global__ void __launch_bounds__(128) modified_1d(const __grid_constant__ Schem
   }
   double w = 2.0;  // w[0] = 2, w[r] = w[r-1] * dt / 2 / r
   ck_tables_1d<MM>(P, Tp, Tv, [&](int r, const double (&Pr)[n], const double (&Vr)[n]) {
-    if (r > 0) w = __ddiv_rn(__ddiv_rn(__dmul_rn(w, P.dt), 2.0), static_cast<double>(r));
+    if (r > 0) w = __ddiv_rn(__dmul_rn(__dmul_rn(w, P.dt), 0.5), static_cast<double>(r));  // (w dt) / 2 == (w dt) * 0.5 exactly
 #pragma unroll
     for (int s2 = 0; s2 < n1; ++s2) {
       if ((s2 % 2 == 0) == (r % 2 == 1)) {  // even s: odd levels; odd s: even levels
@@ -512,7 +520,7 @@ __global__ void __launch_bounds__(128) dual_hermite_1d(const __grid_constant__ S
   const int ri = PASS == 0 ? (j + 1 == P.K ? 0 : j + 1) : j;
   double Tp[n], Tv[n];
   reconstruct_pv_1d<MM>(P, li, ri, Tp, Tv);
-  const double tau = __ddiv_rn(P.dt, 2.0);
+  const double tau = __dmul_rn(P.dt, 0.5);  // dt / 2 exactly
   double op[n1], ov[n1];
 #pragma unroll
   for (int s2 = 0; s2 < n1; ++s2) op[s2] = ov[s2] = 0.0;
