@@ -287,9 +287,14 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   uint32_t rphase = 0, tphase = 0;
   // TMA boxes need: no x wrap / mirror inside the row, the two source rows
   // consecutive and unmirrored
-  const bool tma_rows = P.tma && (P.pre ? (x0 >= 2 && x0 + TXC <= P.sNx) : (x0 + RAWX <= P.sNx)) &&
-                        !__syncthreads_or(mx_lane || mx_last) && (P.pre ? x0 - 1 + TXC < P.K[0] : true) && !my0 &&
-                        !my1 && yo1 == yo0 + P.sNx;
+  const bool xmirror = __syncthreads_or(mx_lane || mx_last);  // block-wide, evaluated by every thread
+#ifdef HLF_EXP_NORAW
+  const bool tma_rows = false;  // ablation build: no raw loads, so nothing to wait for
+  (void)xmirror;
+#else
+  const bool tma_rows = P.tma && (P.pre ? (x0 >= 2 && x0 + TXC <= P.sNx) : (x0 + RAWX <= P.sNx)) && !xmirror &&
+                        (P.pre ? x0 - 1 + TXC < P.K[0] : true) && !my0 && !my1 && yo1 == yo0 + P.sNx;
+#endif
   if (tid == 0) {
     mbar_init(&rawbar[0], 1);
     mbar_init(&rawbar[1], 1);
