@@ -374,7 +374,7 @@ def test_z_slabs_on_one_gpu_match_single_domain(m, overlap):
 @pytest.mark.parametrize("m", [1, 2, 3, 4])
 @pytest.mark.parametrize("boundary", [[0, 0], [1, 1], [0, 1], [1, 0]])
 def test_parity_2d_tiled_kernel(m, boundary):
-    # crosses a partial 32-cell x tile and two 64-row y chunks
+    # crosses a partial 32-cell x tile and three 32-row y chunks
     g, o = make_pair(2, m, [40, 70], boundary=boundary, seed=90 + m)
     assert g.kernel_variant == 1
     run_both(g, o, 5, 0.3 * g.grid.h)
