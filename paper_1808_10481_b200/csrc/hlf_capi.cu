@@ -44,8 +44,10 @@ struct hlf_solver {
   int* flag_host = nullptr;
   double* errbuf = nullptr;     // hlf_error_separable accumulator (device) and its host copy
   double* errbuf_host = nullptr;
-  double* staging = nullptr;
+  double* staging[2] = {nullptr, nullptr};  // double-buffered host-transfer staging
   size_t staging_bytes = 0;
+  cudaStream_t xstream = nullptr;           // copy stream of hlf_set_field / hlf_get_field
+  cudaEvent_t copy_done[2] = {nullptr, nullptr}, perm_done[2] = {nullptr, nullptr};
   int64_t launches = 0;
   int variant = 0;
   std::string err;
@@ -151,19 +153,30 @@ int ipow(int b, int e) {
 bool valid_field(const hlf_solver* s, int f) { return f >= 0 && f < s->nfields; }
 
 hlf_status ensure_staging(hlf_solver* s, size_t bytes) {
+  if (!s->xstream) {
+    HLF_CUDA(s, cudaStreamCreateWithFlags(&s->xstream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      HLF_CUDA(s, cudaEventCreateWithFlags(&s->copy_done[b], cudaEventDisableTiming));
+      HLF_CUDA(s, cudaEventCreateWithFlags(&s->perm_done[b], cudaEventDisableTiming));
+    }
+  }
   if (s->staging_bytes >= bytes) return HLF_OK;
-  if (s->staging) cudaFree(s->staging);
-  s->staging = nullptr;
+  for (double*& b : s->staging) {
+    if (b) cudaFree(b);
+    b = nullptr;
+  }
   s->staging_bytes = 0;
-  HLF_CUDA(s, cudaMalloc(&s->staging, bytes));
+  HLF_CUDA(s, cudaMalloc(&s->staging[0], bytes));
+  HLF_CUDA(s, cudaMalloc(&s->staging[1], bytes));
   s->staging_bytes = bytes;
   return HLF_OK;
 }
 
 constexpr size_t kChunkBytes = size_t(256) << 20;
 
-// host AoS [node][per] <-> device SoA [zoff+z][per][y][x], through a device
-// staging chunk (one H2D/D2H copy + one permute kernel per chunk)
+// host AoS [node][per] <-> device SoA [zoff+z][per][y][x], through two device
+// staging chunks: the PCIe copy of chunk i (copy stream) overlaps the permute
+// kernel of chunk i-1 (solver stream), ordered by per-buffer events
 hlf_status transfer(hlf_solver* s, double* dev, const int* N, int per, int64_t layer, int zoff,
                     double* host, bool to_device) {
   const int64_t nodes = static_cast<int64_t>(N[0]) * N[1] * N[2];
@@ -171,20 +184,37 @@ hlf_status transfer(hlf_solver* s, double* dev, const int* N, int per, int64_t l
   hlf_status st = ensure_staging(s, std::min<int64_t>(nodes, chunk_nodes) * per * sizeof(double));
   if (st != HLF_OK) return st;
   const int64_t coef = static_cast<int64_t>(N[0]) * N[1];
-  for (int64_t n0 = 0; n0 < nodes; n0 += chunk_nodes) {
+  // both buffers start free (and, for downloads, after the work queued on the solver stream)
+  for (int b = 0; b < 2; ++b) {
+    HLF_CUDA(s, cudaEventRecord(s->perm_done[b], s->stream));
+    HLF_CUDA(s, cudaEventRecord(s->copy_done[b], s->stream));
+  }
+  int i = 0;
+  for (int64_t n0 = 0; n0 < nodes; n0 += chunk_nodes, ++i) {
+    const int b = i & 1;
+    double* stg = s->staging[b];
     const int64_t cnt = std::min(chunk_nodes, nodes - n0);
     const size_t bytes = static_cast<size_t>(cnt) * per * sizeof(double);
     if (to_device) {
-      HLF_CUDA(s, cudaMemcpyAsync(s->staging, host + n0 * per, bytes, cudaMemcpyHostToDevice, s->stream));
-      s->launches += hlfk::launch_aos_to_soa(s->staging, dev, n0, cnt, per, N[0], N[1], N[2], layer, coef,
-                                             zoff, s->stream);
+      HLF_CUDA(s, cudaStreamWaitEvent(s->xstream, s->perm_done[b], 0));  // buffer b consumed
+      HLF_CUDA(s, cudaMemcpyAsync(stg, host + n0 * per, bytes, cudaMemcpyHostToDevice, s->xstream));
+      HLF_CUDA(s, cudaEventRecord(s->copy_done[b], s->xstream));
+      HLF_CUDA(s, cudaStreamWaitEvent(s->stream, s->copy_done[b], 0));
+      s->launches += hlfk::launch_aos_to_soa(stg, dev, n0, cnt, per, N[0], N[1], N[2], layer, coef, zoff,
+                                             s->stream);
+      HLF_CUDA(s, cudaEventRecord(s->perm_done[b], s->stream));
     } else {
-      s->launches += hlfk::launch_soa_to_aos(dev, s->staging, n0, cnt, per, N[0], N[1], N[2], layer, coef,
-                                             zoff, s->stream);
-      HLF_CUDA(s, cudaMemcpyAsync(host + n0 * per, s->staging, bytes, cudaMemcpyDeviceToHost, s->stream));
+      HLF_CUDA(s, cudaStreamWaitEvent(s->stream, s->copy_done[b], 0));  // buffer b drained to the host
+      s->launches += hlfk::launch_soa_to_aos(dev, stg, n0, cnt, per, N[0], N[1], N[2], layer, coef, zoff,
+                                             s->stream);
+      HLF_CUDA(s, cudaEventRecord(s->perm_done[b], s->stream));
+      HLF_CUDA(s, cudaStreamWaitEvent(s->xstream, s->perm_done[b], 0));
+      HLF_CUDA(s, cudaMemcpyAsync(host + n0 * per, stg, bytes, cudaMemcpyDeviceToHost, s->xstream));
+      HLF_CUDA(s, cudaEventRecord(s->copy_done[b], s->xstream));
     }
     HLF_CUDA(s, cudaGetLastError());
   }
+  HLF_CUDA(s, cudaStreamSynchronize(s->xstream));
   HLF_CUDA(s, cudaStreamSynchronize(s->stream));
   return HLF_OK;
 }
@@ -439,7 +469,13 @@ void hlf_destroy(hlf_solver* s) {
   if (s->flag_host) cudaFreeHost(s->flag_host);
   if (s->errbuf) cudaFree(s->errbuf);
   if (s->errbuf_host) cudaFreeHost(s->errbuf_host);
-  if (s->staging) cudaFree(s->staging);
+  for (double* b : s->staging)
+    if (b) cudaFree(b);
+  if (s->xstream) cudaStreamDestroy(s->xstream);
+  for (int b = 0; b < 2; ++b) {
+    if (s->copy_done[b]) cudaEventDestroy(s->copy_done[b]);
+    if (s->perm_done[b]) cudaEventDestroy(s->perm_done[b]);
+  }
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
 }
