@@ -138,13 +138,17 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
   constexpr int NTT = MX ? 1 : NT;     // target fields
   constexpr int RAW = F * RAWX;
   constexpr int RAWS = (RAW + 2 + 15) / 16 * 16;  // raw stage stride (128 B multiple, pre-shift spare)
+  // raw stages per source: the merged launch single-buffers its two sources so
+  // that four CTAs fit an SM; its next row is then issued after the X stage
+  // (it lands during the Y + CK stage)
+  constexpr int RST = MX ? 1 : 2;
   constexpr int RING = n * n1 * TXC;
   constexpr int TGT = NTT * F * TXC;
   extern __shared__ __align__(128) double smem_raw[];
   // 128 B aligned base by offset arithmetic (keeps the accesses LDS/STS)
   double* smem = smem_raw + ((128u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 127u)) & 127u) / 8u;
   double* rawbuf = smem + P.pre;       // [source][2 stages]; node 0 of a row at stage base + pre
-  double* ring0 = smem + 2 * NS * RAWS;
+  double* ring0 = smem + RST * NS * RAWS;
   double* ring1 = ring0 + RING;
   double* ringb0 = ring1 + RING;       // MX: x-lines of V_y (ring A = ring0/1 holds V_x's)
   double* ringb1 = ringb0 + (MX ? RING : 0);
@@ -210,14 +214,15 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
         fence_proxy_async();
 #pragma unroll
         for (int si = 0; si < NS; ++si)
-          tma_box3(rawbuf + (si * 2 + (sr & 1)) * RAWS - P.pre, &P.tmap[si], x0 - 2 * P.pre, q, &rawbar[sr & 1]);
+          tma_box3(rawbuf + (si * RST + (sr & (RST - 1))) * RAWS - P.pre, &P.tmap[si], x0 - 2 * P.pre, q,
+                   &rawbar[sr & 1]);
       }
       cp_async_commit();
       return;
     }
 #pragma unroll
     for (int si = 0; si < NS; ++si) {
-      double* raw = rawbuf + (si * 2 + (sr & 1)) * RAWS;
+      double* raw = rawbuf + (si * RST + (sr & (RST - 1))) * RAWS;
       const double* rowbase = (si ? P.src2 : P.src) + static_cast<int64_t>(q) * P.sNx;
       for (int f = warp; f < F; f += NWARP) cp_async8(raw + f * RAWX + lane, rowbase + f * P.s_plane + xo_lane);
       if (tid < F) cp_async8(raw + tid * RAWX + TXC, rowbase + tid * P.s_plane + xo_last);
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
     (void)ymap(sr, my);
     if (!my && !xwall) return;
     for (int si = 0; si < NS; ++si) {
-      double* raw = rawbuf + (si * 2 + (sr & 1)) * RAWS;
+      double* raw = rawbuf + (si * RST + (sr & (RST - 1))) * RAWS;
       const int comp = MX ? si : P.comp;
       for (int e = tid; e < RAW; e += NTHREADS) {
         const int f = e / RAWX, sx = e - f * RAWX;
@@ -284,14 +289,14 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
     __syncthreads();
     fix_raw(snew);
     __syncthreads();
-    if (j + 1 < j1) issue_raw(snew + 1);
+    if (RST == 2 && j + 1 < j1) issue_raw(snew + 1);
     if (j + 1 < j1) issue_targets(j + 1);
-    const double* raw = rawbuf + (snew & 1) * RAWS;
+    const double* raw = rawbuf + (snew & (RST - 1)) * RAWS;
     if constexpr (MX) {
       // V_x with the shifted x rows into ring A, V_y into ring B
       for (int task = warp; task < 4 * n1; task += NWARP) {
         const int si = task >= 2 * n1, tk = task - si * 2 * n1, ly = tk >> 1, px = tk & 1;
-        if (si) x_task<MM>(px, P, raw + 2 * RAWS + ly * RAWX + lane, rnb + ly * TXC + lane);
+        if (si) x_task<MM>(px, P, raw + RST * RAWS + ly * RAWX + lane, rnb + ly * TXC + lane);
         else x_task_sh<MM>(px, P, raw + ly * RAWX + lane, rn + ly * TXC + lane);
       }
     } else {
@@ -301,6 +306,7 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
       }
     }
     __syncthreads();
+    if (RST == 1 && j + 1 < j1) issue_raw(snew + 1);  // single raw stage: X is done with it
     if (work && P.tma_t) {
       mbar_wait(&tgtbar[j & 1], (tphase >> (j & 1)) & 1);
       tphase ^= 1u << (j & 1);
@@ -366,7 +372,8 @@ int launch_one(T2Params T, cudaStream_t st) {
           (NS == 1 || encode_map(&T.tmap[1], T.src2, T.sNx, T.sNy, F, T.s_plane, RAWX));
   T.tma_t = want;
   for (int t = 0; t < NTT && T.tma_t; ++t) T.tma_t = encode_map(&T.tmapT[t], T.dst[t], T.tNx, T.tNy, F, T.t_plane, TXC);
-  const size_t smem = sizeof(double) * (2 * NS * RAWS + 2 * NS * n * n1 * TXC + 2 * NTT * F * TXC) + 128;
+  constexpr int RST = NT == 3 ? 1 : 2;
+  const size_t smem = sizeof(double) * (RST * NS * RAWS + 2 * NS * n * n1 * TXC + 2 * NTT * F * TXC) + 128;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tiled2d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
