@@ -138,10 +138,11 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
   constexpr int NTT = MX ? 1 : NT;     // target fields
   constexpr int RAW = F * RAWX;
   constexpr int RAWS = (RAW + 2 + 15) / 16 * 16;  // raw stage stride (128 B multiple, pre-shift spare)
-  // raw stages per source: the merged launch single-buffers its two sources so
-  // that four CTAs fit an SM; its next row is then issued after the X stage
-  // (it lands during the Y + CK stage)
-  constexpr int RST = MX ? 1 : 2;
+  // raw stages per source: the merged launch (and m = 4) single-buffers its
+  // sources so that one more CTA fits an SM; the next row is then issued after
+  // the X stage (it lands during the Y + CK stage).  Merged m = 3: +7 %,
+  // m = 4: +3 %; m <= 2 single launches keep two stages (-3 % otherwise).
+  constexpr int RST = (MX || MM >= 4) ? 1 : 2;
   constexpr int RING = n * n1 * TXC;
   constexpr int TGT = NTT * F * TXC;
   extern __shared__ __align__(128) double smem_raw[];
@@ -372,7 +373,7 @@ int launch_one(T2Params T, cudaStream_t st) {
           (NS == 1 || encode_map(&T.tmap[1], T.src2, T.sNx, T.sNy, F, T.s_plane, RAWX));
   T.tma_t = want;
   for (int t = 0; t < NTT && T.tma_t; ++t) T.tma_t = encode_map(&T.tmapT[t], T.dst[t], T.tNx, T.tNy, F, T.t_plane, TXC);
-  constexpr int RST = NT == 3 ? 1 : 2;
+  constexpr int RST = (NT == 3 || MM >= 4) ? 1 : 2;
   const size_t smem = sizeof(double) * (RST * NS * RAWS + 2 * NS * n * n1 * TXC + 2 * NTT * F * TXC) + 128;
   static bool configured = false;
   if (!configured) {
