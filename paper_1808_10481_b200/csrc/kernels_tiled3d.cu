@@ -57,16 +57,16 @@ struct Cfg {
   template <int NT>
   static constexpr int NTGT = NT == 2 ? 1 : NT;
   template <int NT>
-  static constexpr int NRAW = NT == 2 ? 2 : ((NT == 1 && MM < 3) ? 2 : 1);
+  static constexpr int NRAW = NT == 2 ? 2 : ((NT == 1 && MM == 1) ? 2 : 1);
   template <int NT>
   static constexpr int TGT = NTGT<NT> * F * TXC;
-  // NT == 1 (pressure), m < 3: the raw stage is double-buffered so the source
-  // layer gets a whole iteration to land (+18 % at m = 1).  At m = 3 the 8-warp
-  // CTA has no shared memory left for it.  Targets are single-buffered: every
+  // NT == 1 (pressure), m = 1: the raw stage is double-buffered so the source
+  // layer gets a whole iteration to land (+11 % at m = 1 with TMA loads; at
+  // m = 2 a single stage is 1.7 % faster, at m = 3 there is no room for it).  Targets are single-buffered: every
   // staged target value is read by exactly one lane, which reloads its slots
   // for the next layer right after its epilogue (no barrier needed).
   template <int NT>
-  static constexpr int NBUF = (NT == 1 && MM < 3) ? 2 : 1;
+  static constexpr int NBUF = (NT == 1 && MM == 1) ? 2 : 1;
   template <int NT>
   static constexpr int SMEM_DOUBLES = NRAW<NT> * RAWS + 2 * RING + TGT<NT>;
 };
