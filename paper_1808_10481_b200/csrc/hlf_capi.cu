@@ -8,6 +8,7 @@
 // (:121-129), ConfigError for bad m / grid / field count (config.cpp:27-32,
 // grid.cpp:10-26).
 #include <climits>
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -27,6 +28,7 @@ struct hlf_solver {
   double x_min[3] = {0, 0, 0};
   double h = 1.0, ap = -1.0, av = -1.0;
   bool variable = false;
+  bool m_mirror = true;  // M_R = diag((-1)^r) M_L diag((-1)^l): the fast kernels use M_L only
   bool z_slab = false;
   int scheme = HLF_SCHEME_LEAPFROG;
   int nfields = 2;              // d + 1, or 4 for the 1D alternative schemes
@@ -279,6 +281,14 @@ void fill_weights(const hlf_solver* s, hlfk::HalfKind kind, HalfParams& P) {
 // zlo/zhi: target layers [zlo, zhi) of a 3D half step (-1: all).  A range is
 // the full launch with both field bases shifted by zlo layers, so every kernel
 // runs it unchanged.
+// variant 1 = the fast kernels: tiled3d / tiled2d (constant coefficients),
+// var2d (2D with per-node ap jets)
+bool tiled_available(const hlf_solver* s) {
+  if (!s->m_mirror) return false;
+  if (s->variable) return s->d == 2 && hlfk::var2d_supported(s->m);
+  return (s->d == 3 && hlfk::tiled3d_supported(s->m)) || (s->d == 2 && hlfk::tiled2d_supported(s->m));
+}
+
 hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0, int zhi = -1) {
   if (s->scheme != HLF_SCHEME_LEAPFROG)
     return fail(s, HLF_CONFIG_ERROR, "half steps belong to the leapfrog scheme; use hlf_step");
@@ -329,6 +339,8 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
     launched = hlfk::launch_half_tiled3d(s->m, kind, P, s->stream);
   else if (s->variant == 1 && !s->variable && s->d == 2 && hlfk::tiled2d_supported(s->m))
     launched = hlfk::launch_half_tiled2d(s->m, kind, P, s->stream);
+  else if (s->variant == 1 && s->variable && s->d == 2 && hlfk::var2d_supported(s->m))
+    launched = hlfk::launch_half_var2d(s->m, kind, P, s->stream);
   if (launched == -2 || launched < 0 && s->variant != 1)  // -2: custom M / planes too large for the tiled kernel
     launched = hlfk::launch_half_generic(s->d, s->m, s->variable, kind, P, s->stream);
   if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
@@ -416,6 +428,18 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
   } else {
     build_M(s->m, s->M, nullptr);
   }
+  {
+    // a caller-supplied M without the mirror symmetry of A (interpolation.cpp:29-38)
+    // runs on the generic kernel, which applies all n x n entries
+    double mx = 0.0, dev = 0.0;
+    for (double v : s->M) mx = std::max(mx, std::fabs(v));
+    for (int r = 0; r < s->n; ++r)
+      for (int l = 0; l < s->n1; ++l) {
+        const double sg = ((r + l) & 1) ? -1.0 : 1.0;
+        dev = std::max(dev, std::fabs(s->M[r * s->n + s->n1 + l] - sg * s->M[r * s->n + l]));
+      }
+    s->m_mirror = dev <= 1e-13 * mx;
+  }
   auto bail = [&](hlf_status st) {
     g_create_error = s->err;
     hlf_destroy(s);
@@ -451,8 +475,7 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
   if (e != cudaSuccess) return bail(cuda_fail(s, e, "flag init"));
   e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) return bail(cuda_fail(s, e, "sync"));
-  s->variant = !s->variable && ((d == 3 && hlfk::tiled3d_supported(s->m)) || (d == 2 && hlfk::tiled2d_supported(s->m)))
-                   ? 1 : 0;
+  s->variant = tiled_available(s) ? 1 : 0;
   *out = s;
   return HLF_OK;
 }
@@ -820,8 +843,7 @@ int hlf_kernel_variant(const hlf_solver* s) { return s ? s->variant : -1; }
 
 hlf_status hlf_set_kernel_variant(hlf_solver* s, int variant) {
   if (!s) return HLF_INVALID_ARGUMENT;
-  if (variant == 1 && !(!s->variable && ((s->d == 3 && hlfk::tiled3d_supported(s->m)) ||
-                                          (s->d == 2 && hlfk::tiled2d_supported(s->m)))))
+  if (variant == 1 && !tiled_available(s))
     return fail(s, HLF_CONFIG_ERROR, "tiled kernel not available for this configuration");
   if (variant != 0 && variant != 1) return fail(s, HLF_INVALID_ARGUMENT, "unknown variant");
   s->variant = variant;

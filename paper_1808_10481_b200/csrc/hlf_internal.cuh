@@ -87,6 +87,9 @@ int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t 
 bool tiled3d_supported(int m);
 int launch_half_tiled2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
 bool tiled2d_supported(int m);
+// 2D with per-node ap jets (variable c^2), m = 1..4
+int launch_half_var2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
+bool var2d_supported(int m);
 int launch_fill(const FillParams& p, cudaStream_t st);
 // field - amp prod sin_jet -> err[0] += sum of squared value errors, err[1] = max |jet error|
 int launch_error(const FillParams& p, cudaStream_t st);

@@ -167,6 +167,77 @@ def test_parity_variable_speed(d, m, boundary):
     compare(g, o, d)
 
 
+def set_both_coeff(g, o, jets_of):
+    for grid, dual in ((0, False), (1, True)):
+        jets = jets_of(grid, dual)
+        g.set_coeff(grid, jets)
+        o.set_coeff(grid, 0, jets)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+@pytest.mark.parametrize("boundary", [[0, 0], [1, 1], [1, 0]])
+def test_parity_2d_variable_kernel(m, boundary):
+    # var2d (per-node ap jets): K = 13 x 11 leaves a partial CTA and, at m = 2
+    # and 4, idle lanes; the c^2 jets of config 3
+    K = [13, 11]
+    g, o = make_pair(2, m, K, boundary=boundary, variable=True, seed=80 + m)
+    assert g.kernel_variant == 1
+    set_both_coeff(g, o, lambda grid, dual: c2_jets(2, K, g.grid.h, 2 * m + 2, boundary, dual))
+    run_both(g, o, 4, 0.2 * g.grid.h)
+    compare(g, o, 2)
+
+
+@pytest.mark.parametrize("m", [1, 3, 4])
+def test_parity_2d_variable_kernel_random_jets(m):
+    # dense random ap jets: every entry of the truncated products contributes,
+    # so a wrong region (rows / columns skipped) cannot hide
+    K, boundary = [9, 12], [1, 1]
+    g, o = make_pair(2, m, K, boundary=boundary, variable=True, seed=90 + m)
+    rng = np.random.default_rng(7 + m)
+    n = 2 * m + 2
+
+    def jets(grid, dual):
+        a = rng.standard_normal((g.field_nodes(1 if dual else 0), n * n)) * 0.3
+        a *= 0.7 ** np.add.outer(np.arange(n), np.arange(n)).ravel()
+        a[:, 0] -= 1.0
+        return a
+
+    set_both_coeff(g, o, jets)
+    run_both(g, o, 4, 0.2 * g.grid.h)
+    compare(g, o, 2)
+
+
+def test_variable_kernel_equals_generic_long_run():
+    # var2d reorders the arithmetic (FMA, sum/difference M, Lap instead of
+    # grad-then-div); over a long run it stays at the roundoff floor of the
+    # faithful generic kernel
+    K, boundary, m = [70, 45], [1, 1], 3
+    runs = []
+    for variant in (1, 0):
+        g, _ = make_pair(2, m, K, boundary=boundary, variable=True, seed=11)
+        for grid, dual in ((0, False), (1, True)):
+            g.set_coeff(grid, c2_jets(2, K, g.grid.h, 2 * m + 2, boundary, dual))
+        g.kernel_variant = variant
+        g.set_times(0.0, 0.005, 0.01)
+        g.advance_n(40)
+        runs.append([g.get_field(f) for f in range(3)])
+    for a, b in zip(*runs):
+        assert rel_err(a, b) <= 1e-10
+
+
+def test_asymmetric_M_disables_fast_kernels():
+    # the fast kernels apply M through its left half (the mirror symmetry of
+    # A); a caller-supplied M without it must run on the generic kernel
+    m, K = 2, [12, 10]
+    M = H.build_interp_operator(m).M.copy()
+    M[1, 2 * m + 1] *= 1.0 + 1e-9
+    for variable in (False, True):
+        g = H.Stepper(H.Grid([-1.0] * 2, 2.0 / K[0], tuple(K)), m, M=M, variable_ap=variable)
+        assert g.kernel_variant == 0
+        with pytest.raises(H.ConfigError):
+            g.kernel_variant = 1
+
+
 def test_1d_variable_coefficients_vs_compiled_reference():
     if not O.ref_available():
         pytest.skip("compiled reference not present")
