@@ -19,15 +19,20 @@
 // time from the target box by "grow" (Lap reads q + 2e_x and q + 2e_y); at
 // m = 3 this is 2232 multiply-adds per pressure cell instead of 5184.
 //
-// Layout: G = m + 1 threads ("quad" at m = 3) per cell, 32 / G cells per warp,
-// 4 warps per CTA, no inter-warp sharing (only __syncwarp).  Each cell owns
-// three n x n jets in shared memory (ap, X = the derivative term, P = the
-// level), rows padded to n + 2 doubles; thread t owns jet rows t and
-// n - 1 - t, so the target rows 0..m are one per thread.  The product of a
-// row is a sum of 1D causal convolutions of ap rows with X rows (rows in
-// registers, LDS.128), the reconstruction uses the sum/difference form of M
-// (M_R = diag((-1)^r) M_L diag((-1)^l), interpolation.cpp:29-48).
+// Layout: two threads per cell, 16 cells per warp, 2 warps per CTA.  Thread t
+// owns the jet rows qx = t, t + 2, t + 4, ... of every level, so the level
+// P_k lives in its registers and Lap P_k (rows qx and qx + 2) is
+// thread-local; only X (the operand of the next product, all rows) and the
+// ap jet sit in shared memory (rows padded to an odd number of 16 B slots,
+// cells 2 slots apart: the LDS.128 row loads of a warp are conflict-free).
+// The product of a row is a sum of 1D causal convolutions of ap rows with X
+// rows; every ap row a thread loads serves all of its output rows.  The x
+// derivatives of the velocity outputs and of div V_0 read the partner
+// thread's rows through one shuffle per value.  The reconstruction uses the
+// sum/difference form of M (M_R = diag((-1)^r) M_L diag((-1)^l),
+// interpolation.cpp:29-48).
 #include <cstring>
+#include <utility>
 
 #include "hlf_internal.cuh"
 
@@ -35,22 +40,20 @@ namespace hlfk {
 namespace v2d {
 namespace {
 
-constexpr int NTHREADS = 128;
+constexpr int NTHREADS = 64;
+constexpr unsigned FULL = 0xffffffffu;
 
 template <int MM>
 struct Shape {
-  static constexpr int n1 = MM + 1, n = 2 * MM + 2, G = MM + 1;
-  // Bank mapping: LDS.128 serves eight 16 B slots per wavefront.  Rows are an
-  // odd number of slots apart (a cell's threads read distinct rows) and cells
-  // an odd number of slots apart too (the broadcast ap rows of the 8 cells of
-  // a warp and the 32 distinct X rows then spread evenly over the slots).
-  static constexpr int RS = ((n + 2) / 2) % 2 ? n + 2 : n + 4;  // padded row (doubles)
+  static constexpr int n1 = MM + 1, n = 2 * MM + 2;
+  static constexpr int NJ = MM + 1;                              // rows per thread
+  static constexpr int NS = MM / 2 + 1;                          // target rows per thread (max)
+  static constexpr int RS = ((n + 2) / 2) % 2 ? n + 2 : n + 4;   // padded row: odd number of 16 B slots
   static constexpr int AS = n * RS;                              // one jet
-  static constexpr int CS = (3 * AS + 15) / 16 * 16 + 2;         // cell stride: 16 B mod 128 B
-  static constexpr int CPW = 32 / G;                      // cells per warp
-  static constexpr int SPW = CPW + (32 % G ? 1 : 0);      // + a dummy slot for idle lanes
+  static constexpr int CS = (2 * AS + 15) / 16 * 16 + 4;         // cell stride: 2 slots mod 8
+  static constexpr int CPW = 16;
   static constexpr int CPC = CPW * (NTHREADS / 32);
-  static constexpr int SMEM = (NTHREADS / 32) * SPW * CS * 8;
+  static constexpr int SMEM = CPC * CS * 8;
 };
 
 // lim[k][r]: the largest qy of row r needed at level k (-1: row not needed)
@@ -77,8 +80,11 @@ struct Regions {
         lim[k][r] = v;
       }
   }
-  __host__ __device__ constexpr int lo(int k) const { return lim[k][0]; }
-  __host__ __device__ constexpr int hi(int k) const { return lim[k][n / 2]; }
+  // limit of thread-row j (rows 2j and 2j + 1 of the two threads)
+  __host__ __device__ constexpr int row_pair(int k, int j) const {
+    const int a = lim[k][2 * j], b = lim[k][2 * j + 1];
+    return a > b ? a : b;
+  }
   __host__ __device__ constexpr int last_row(int k) const {
     int r = -1;
     for (int q = 0; q < n; ++q)
@@ -87,148 +93,10 @@ struct Regions {
   }
 };
 
-// row-vector loads of L + 1 doubles (pairs; RS = n + 2 keeps the pad in range)
-template <int L>
-__device__ __forceinline__ void load_row(double (&v)[L + 2], const double* p) {
-#pragma unroll
-  for (int i = 0; i <= L; i += 2) {
-    const double2 t = *reinterpret_cast<const double2*>(p + i);
-    v[i] = t.x;
-    v[i + 1] = t.y;
-  }
-}
-
-// acc[qy] += sum_{iy <= qy} a[iy] x[qy - iy], qy <= L (truncated 1D product)
-template <int L>
-__device__ __forceinline__ void conv_row(double (&acc)[L + 1], const double* a, const double* x) {
-  double av[L + 2], xv[L + 2];
-  load_row<L>(av, a);
-  load_row<L>(xv, x);
-#pragma unroll
-  for (int qy = 0; qy <= L; ++qy)
-#pragma unroll
-    for (int iy = 0; iy <= qy; ++iy) acc[qy] = fma(av[iy], xv[qy - iy], acc[qy]);
-}
-
-template <int L>
-__device__ __forceinline__ void store_row(double* p, const double (&v)[L + 1]) {
-#pragma unroll
-  for (int i = 0; i <= L; ++i) p[i] = v[i];
-}
-
-// one level's product P = ap (.) X on the rows this thread owns
-template <int MM, int KIND, int K>
-__device__ __forceinline__ void product(const HalfParams& P, const double* A, const double* X, double* Pj,
-                                        int t, double (&tgt)[MM + 1]) {
-  using S = Shape<MM>;
-  constexpr Regions<MM, KIND> R{};
-  constexpr int Llo = R.lo(K), Lhi = R.hi(K), last = R.last_row(K);
-  {
-    double acc[Llo + 1];
-#pragma unroll
-    for (int i = 0; i <= Llo; ++i) acc[i] = 0.0;
-    for (int ix = 0; ix <= t; ++ix) conv_row<Llo>(acc, A + ix * S::RS, X + (t - ix) * S::RS);
-    store_row<Llo>(Pj + t * S::RS, acc);
-    if constexpr (KIND == PRE && (K & 1)) {
-#pragma unroll
-      for (int b = 0; b <= MM; ++b) tgt[b] = fma(P.w[K], acc[b], tgt[b]);
-    }
-  }
-  if constexpr (Lhi >= 0) {
-    const int r = S::n - 1 - t;
-    if (r <= last) {
-      double acc[Lhi + 1];
-#pragma unroll
-      for (int i = 0; i <= Lhi; ++i) acc[i] = 0.0;
-      for (int ix = 0; ix <= r; ++ix) conv_row<Lhi>(acc, A + ix * S::RS, X + (r - ix) * S::RS);
-      store_row<Lhi>(Pj + r * S::RS, acc);
-    }
-  }
-}
-
-// X = av Lap P on one row r (qy <= L): (P[r+2][qy] (r+1)(r+2) + P[r][qy+2] (qy+1)(qy+2)) av / h^2
-template <int MM, int L>
-__device__ __forceinline__ void lap_row(const double* Pj, double* X, int r, double c) {
-  using S = Shape<MM>;
-  constexpr int n = S::n;
-  constexpr int LO = L + 2 < n - 1 ? L + 2 : n - 1;  // own-row entries read
-  double own[LO + 2];
-  load_row<LO>(own, Pj + r * S::RS);
-  double out[L + 1];
-  const double fx = static_cast<double>((r + 1) * (r + 2));
-  if (r + 2 < n) {
-    double up[L + 2];
-    load_row<L>(up, Pj + (r + 2) * S::RS);
-#pragma unroll
-    for (int qy = 0; qy <= L; ++qy) out[qy] = up[qy] * fx;
-  } else {
-#pragma unroll
-    for (int qy = 0; qy <= L; ++qy) out[qy] = 0.0;
-  }
-#pragma unroll
-  for (int qy = 0; qy <= L; ++qy)
-    if (qy + 2 < n) out[qy] = fma(own[qy + 2], static_cast<double>((qy + 1) * (qy + 2)), out[qy]);
-#pragma unroll
-  for (int qy = 0; qy <= L; ++qy) out[qy] *= c;
-  store_row<L>(X + r * S::RS, out);
-}
-
-template <int MM, int KIND, int K>
-__device__ __forceinline__ void laplacian(const double* Pj, double* X, int t, double c) {
-  using S = Shape<MM>;
-  constexpr Regions<MM, KIND> R{};
-  constexpr int Llo = R.lo(K), Lhi = R.hi(K), last = R.last_row(K);
-  lap_row<MM, Llo>(Pj, X, t, c);
-  if constexpr (Lhi >= 0) {
-    const int r = S::n - 1 - t;
-    if (r <= last) lap_row<MM, Lhi>(Pj, X, r, c);
-  }
-}
-
-// PRE levels K = 1, 3, .., n - 1: P_K = ap (.) X_K, target += w_K P_K,
-// X_{K+2} = av Lap P_K
-template <int MM, int K>
-__device__ __forceinline__ void pre_levels(const HalfParams& P, const double* A, double* X, double* Pj, int t,
-                                           double c, double (&tgt)[MM + 1]) {
-  product<MM, PRE, K>(P, A, X, Pj, t, tgt);
-  if constexpr (K + 2 < 2 * MM + 2) {
-    __syncwarp();
-    laplacian<MM, PRE, K + 2>(Pj, X, t, c);
-    __syncwarp();
-    pre_levels<MM, K + 2>(P, A, X, Pj, t, c, tgt);
-  }
-}
-
-// VEL levels K = 0, 2, .., n - 2: target_c += w_{K+1} av d_c P_K on the
-// target rows, then X_{K+2} = av Lap P_K and P_{K+2} = ap (.) X_{K+2}
-template <int MM, int K>
-__device__ __forceinline__ void vel_levels(const HalfParams& P, const double* A, double* X, double* Pj, int t,
-                                           double c, double inv_h, double (&tgt)[2][MM + 1]) {
-  using S = Shape<MM>;
-  constexpr int n1 = MM + 1, n = 2 * MM + 2;
-  const double wa = P.w[K + 1] * P.av * inv_h;
-  double up[n1 + 1], own[n1 + 3];
-  load_row<n1 - 1>(up, Pj + (t + 1) * S::RS);
-  load_row<n1 + 1>(own, Pj + t * S::RS);
-  const double fxr = static_cast<double>(t + 1) * wa;
-#pragma unroll
-  for (int b = 0; b < n1; ++b) {
-    tgt[0][b] = fma(up[b], fxr, tgt[0][b]);
-    tgt[1][b] = fma(own[b + 1], static_cast<double>(b + 1) * wa, tgt[1][b]);
-  }
-  if constexpr (K + 2 < n - 1) {
-    laplacian<MM, VEL, K + 2>(Pj, X, t, c);
-    __syncwarp();
-    double unused[MM + 1];
-    product<MM, VEL, K + 2>(P, A, X, Pj, t, unused);
-    __syncwarp();
-    vel_levels<MM, K + 2>(P, A, X, Pj, t, c, inv_h, tgt);
-  }
-}
-
 // sum/difference form of one M application: out[r] = sum_l M[r][l] (L_l + (-1)^{r-l} R_l)
 template <int MM>
-__device__ __forceinline__ void apply_m(const HalfParams& P, const double (&lr)[2 * MM + 2], double (&out)[2 * MM + 2]) {
+__device__ __forceinline__ void apply_m(const HalfParams& P, const double (&lr)[2 * MM + 2],
+                                        double (&out)[2 * MM + 2]) {
   constexpr int n1 = MM + 1, n = 2 * MM + 2;
   double sg[n1], df[n1];
 #pragma unroll
@@ -245,36 +113,203 @@ __device__ __forceinline__ void apply_m(const HalfParams& P, const double (&lr)[
   }
 }
 
+// the row-pair limits as compile-time constants (a constexpr table indexed by
+// an unrolled loop variable would be materialised in local memory)
+template <int MM, int KIND, int K, int J>
+struct RowLim {
+  static constexpr int v = Regions<MM, KIND>{}.row_pair(K, J);
+  static constexpr int last = Regions<MM, KIND>{}.last_row(K);
+};
+
+// acc[J] (row 2J + t) += ap[IX] (*) X[row - IX] when the row is in R_K
+template <int MM, int KIND, int K, int IX, int J>
+__device__ __forceinline__ void product_row(const double (&av)[2 * MM + 4], const double* X, int t,
+                                            double (&acc)[MM + 1][2 * MM + 2]) {
+  using S = Shape<MM>;
+  constexpr int Lj = RowLim<MM, KIND, K, J>::v, last = RowLim<MM, KIND, K, J>::last;
+  if constexpr (Lj >= 0 && 2 * J + 1 >= IX) {
+    const int r = 2 * J + t;
+    if (r >= IX && r <= last) {
+      double xv[S::n + 2];
+#pragma unroll
+      for (int i = 0; i <= Lj; i += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(X + (r - IX) * S::RS + i);
+        xv[i] = v.x;
+        xv[i + 1] = v.y;
+      }
+#pragma unroll
+      for (int qy = 0; qy <= Lj; ++qy)
+#pragma unroll
+        for (int iy = 0; iy <= qy; ++iy) acc[J][qy] = fma(av[iy], xv[qy - iy], acc[J][qy]);
+    }
+  }
+}
+
+template <int MM, int KIND, int K, int IX, int... J>
+__device__ __forceinline__ void product_rows(std::integer_sequence<int, J...>, const double (&av)[2 * MM + 4],
+                                             const double* X, int t, double (&acc)[MM + 1][2 * MM + 2]) {
+  (product_row<MM, KIND, K, IX, J>(av, X, t, acc), ...);
+}
+
+// for IX = 0.. : load ap row IX once, apply it to every row of the thread
+template <int MM, int KIND, int K, int IX>
+__device__ __forceinline__ void product_ix(const double* A, const double* X, int t,
+                                           double (&acc)[MM + 1][2 * MM + 2]) {
+  using S = Shape<MM>;
+  constexpr int last = RowLim<MM, KIND, K, 0>::last;
+  if constexpr (IX <= last) {
+    constexpr int LA = RowLim<MM, KIND, K, IX / 2>::v;  // widest row that uses ap row IX
+    double av[S::n + 2];
+#pragma unroll
+    for (int i = 0; i <= LA; i += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(A + IX * S::RS + i);
+      av[i] = v.x;
+      av[i + 1] = v.y;
+    }
+    product_rows<MM, KIND, K, IX>(std::make_integer_sequence<int, S::NJ>{}, av, X, t, acc);
+    product_ix<MM, KIND, K, IX + 1>(A, X, t, acc);
+  }
+}
+
+template <int MM, int KIND, int K>
+__device__ __forceinline__ void product(const double* A, const double* X, int t, double (&acc)[MM + 1][2 * MM + 2]) {
+  constexpr int n = 2 * MM + 2;
+#pragma unroll
+  for (int j = 0; j <= MM; ++j)
+#pragma unroll
+    for (int q = 0; q < n; ++q) acc[j][q] = 0.0;
+  product_ix<MM, KIND, K, 0>(A, X, t, acc);
+}
+
+// X_K = av Lap P_{K-2} on thread-row J (row r + 2 = acc[J + 1])
+template <int MM, int KIND, int K, int J>
+__device__ __forceinline__ void lap_row(double (&acc)[MM + 1][2 * MM + 2], int t, double c) {
+  constexpr int n = 2 * MM + 2, NJ = MM + 1;
+  constexpr int Lj = RowLim<MM, KIND, K, J>::v;
+  if constexpr (Lj >= 0) {
+    const int r = 2 * J + t;
+    const double fx = static_cast<double>((r + 1) * (r + 2));
+#pragma unroll
+    for (int qy = 0; qy <= Lj; ++qy) {
+      double v = J + 1 < NJ ? acc[J + 1 < NJ ? J + 1 : J][qy] * fx : 0.0;
+      if (qy + 2 < n) v = fma(acc[J][qy + 2 < n ? qy + 2 : qy], static_cast<double>((qy + 1) * (qy + 2)), v);
+      acc[J][qy] = v * c;
+    }
+  }
+}
+
+template <int MM, int KIND, int K, int J>
+__device__ __forceinline__ void store_row(const double (&acc)[MM + 1][2 * MM + 2], double* X, int t) {
+  using S = Shape<MM>;
+  constexpr int Lj = RowLim<MM, KIND, K, J>::v, last = RowLim<MM, KIND, K, J>::last;
+  if constexpr (Lj >= 0) {
+    const int r = 2 * J + t;
+    if (r <= last) {
+#pragma unroll
+      for (int i = 0; i <= Lj; i += 2)
+        *reinterpret_cast<double2*>(X + r * S::RS + i) =
+            make_double2(acc[J][i], i + 1 < S::n ? acc[J][i + 1 < S::n ? i + 1 : i] : 0.0);
+    }
+  }
+}
+
+// Lap in registers (ascending rows: row J + 1 is still P_{K-2} when row J
+// reads it), then the store once the partner has finished reading X
+template <int MM, int KIND, int K, int... J>
+__device__ __forceinline__ void laplacian_store_(std::integer_sequence<int, J...>, double (&acc)[MM + 1][2 * MM + 2],
+                                                 double* X, int t, double c) {
+  (lap_row<MM, KIND, K, J>(acc, t, c), ...);
+  __syncwarp();
+  (store_row<MM, KIND, K, J>(acc, X, t), ...);
+  __syncwarp();
+}
+
+template <int MM, int KIND, int K>
+__device__ __forceinline__ void laplacian_store(double (&acc)[MM + 1][2 * MM + 2], double* X, int t, double c) {
+  laplacian_store_<MM, KIND, K>(std::make_integer_sequence<int, MM + 1>{}, acc, X, t, c);
+}
+
+// PRE levels K = 1, 3, .., n - 1: P_K = ap (.) X_K, target += w_K P_K,
+// X_{K+2} = av Lap P_K
+template <int MM, int K>
+__device__ __forceinline__ void pre_levels(const HalfParams& P, const double* A, double* X, int t, double c,
+                                           double (&acc)[MM + 1][2 * MM + 2], double (&tgt)[MM / 2 + 1][MM + 1]) {
+  product<MM, PRE, K>(A, X, t, acc);
+#pragma unroll
+  for (int s = 0; s <= MM / 2; ++s)
+    if (2 * s + t <= MM) {
+#pragma unroll
+      for (int b = 0; b <= MM; ++b) tgt[s][b] = fma(P.w[K], acc[s][b], tgt[s][b]);
+    }
+  if constexpr (K + 2 < 2 * MM + 2) {
+    laplacian_store<MM, PRE, K + 2>(acc, X, t, c);
+    pre_levels<MM, K + 2>(P, A, X, t, c, acc, tgt);
+  }
+}
+
+// VEL levels K = 0, 2, .., n - 2: target_c += w_{K+1} av d_c P_K on the
+// target rows (d_x reads row r + 1, the partner's), then X_{K+2} = av Lap P_K
+// and P_{K+2} = ap (.) X_{K+2}
+template <int MM, int K>
+__device__ __forceinline__ void vel_levels(const HalfParams& P, const double* A, double* X, int t, double c,
+                                           double inv_h, double (&acc)[MM + 1][2 * MM + 2],
+                                           double (&tgt)[2][MM / 2 + 1][MM + 1]) {
+  constexpr int NJ = MM + 1;
+  const double wa = P.w[K + 1] * P.av * inv_h;
+#pragma unroll
+  for (int s = 0; s <= MM / 2; ++s) {
+    const double fxr = static_cast<double>(2 * s + t + 1) * wa;
+#pragma unroll
+    for (int b = 0; b <= MM; ++b) {
+      // row 2s + t + 1 is the partner's acc[s + t]; we send it our acc[s + 1 - t]
+      const double hi = s + 1 < NJ ? acc[s + 1][b] : 0.0;
+      const double up = __shfl_xor_sync(FULL, t ? acc[s][b] : hi, 1);
+      if (2 * s + t <= MM) {
+        tgt[0][s][b] = fma(up, fxr, tgt[0][s][b]);
+        tgt[1][s][b] = fma(acc[s][b + 1], static_cast<double>(b + 1) * wa, tgt[1][s][b]);
+      }
+    }
+  }
+  if constexpr (K + 2 < 2 * MM + 1) {
+    laplacian_store<MM, VEL, K + 2>(acc, X, t, c);
+    product<MM, VEL, K + 2>(A, X, t, acc);
+    vel_levels<MM, K + 2>(P, A, X, t, c, inv_h, acc, tgt);
+  }
+}
+
 template <int MM, int KIND>
 __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfParams P) {
   using S = Shape<MM>;
-  constexpr int n1 = S::n1, n = S::n, G = S::G;
+  constexpr int n1 = S::n1, n = S::n, NJ = S::NJ, NS = S::NS;
   constexpr int NSRC = KIND == VEL ? 1 : 2;
   constexpr int NOUT = KIND == VEL ? 2 : 1;
   extern __shared__ double smem[];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = lane / G;
-  const int t = lane - q * G;
+  const int q = lane >> 1;
+  const int t = lane & 1;
   const int64_t total = static_cast<int64_t>(P.tNx) * P.tNy;
   const int64_t cell = static_cast<int64_t>(blockIdx.x) * S::CPC + warp * S::CPW + q;
-  const bool live = q < S::CPW && cell < total;
-  double* A = smem + (warp * S::SPW + (q < S::CPW ? q : S::CPW)) * S::CS;
+  const bool live = cell < total;
+  double* A = smem + (warp * S::CPW + q) * S::CS;
   double* X = A + S::AS;
-  double* Pj = X + S::AS;
 
   const int tx = live ? static_cast<int>(cell % P.tNx) : 0;
   const int ty = live ? static_cast<int>(cell / P.tNx) : 0;
   const int64_t tnode = static_cast<int64_t>(ty) * P.tNx + tx;
-  const int rl = t, rh = n - 1 - t;
 
-  // ap jet rows rl, rh -> A  ([E][y][x] planes, e = qx n + qy)
+  // ap jet rows t, t + 2, .. -> A  ([E][y][x] planes, e = qx n + qy)
   {
     const double* ap = P.coeff + tnode;
 #pragma unroll
-    for (int qy = 0; qy < n; ++qy) {
-      A[rl * S::RS + qy] = __ldg(ap + (rl * n + qy) * P.c_coef);
-      A[rh * S::RS + qy] = __ldg(ap + (rh * n + qy) * P.c_coef);
+    for (int j = 0; j < NJ; ++j) {
+      const int r = 2 * j + t;
+#pragma unroll
+      for (int qy = 0; qy < n; qy += 2) {
+        const double a0 = __ldg(ap + (r * n + qy) * P.c_coef);
+        const double a1 = __ldg(ap + (r * n + qy + 1) * P.c_coef);
+        *reinterpret_cast<double2*>(A + r * S::RS + qy) = make_double2(a0, a1);
+      }
     }
   }
   // corner nodes and wall flips (as half_generic): VEL corners t + side,
@@ -303,89 +338,106 @@ __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfPa
     cy[side] = static_cast<int64_t>(qy) * P.sNx;
   }
 
-  double tgt[NOUT][n1];
+  // target rows 2s + t <= m (s < NS)
+  double tgt[NOUT][NS][n1];
 #pragma unroll
   for (int c = 0; c < NOUT; ++c)
 #pragma unroll
-    for (int b = 0; b < n1; ++b) tgt[c][b] = P.dst[c][tnode + (rl * n1 + b) * P.t_coef];
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int b = 0; b < n1; ++b)
+        tgt[c][s][b] = 2 * s + t <= MM ? P.dst[c][tnode + ((2 * s + t) * n1 + b) * P.t_coef] : 0.0;
 
-  double vy[2][n];  // PRE: V_y rows rl, rh of the reconstruction
+  const double inv_h = P.inv_h;
+  double acc[NJ][n];  // this thread's rows of the current level
   // ---- reconstruction (reconstruct_cell_2d, interpolation.cpp:77-113) ----
 #pragma unroll
   for (int comp = 0; comp < NSRC; ++comp) {
     const double* src = P.src[comp];
-    // x sweep of stacked columns rl (sy = 0, b = t) and rh (sy = 1, b = m - t) -> X
+    // x sweep of the stacked columns of y side t (orders b = 0..m) -> X
+    {
+      const int fyt = t ? fy[1] : fy[0];  // (selects: a runtime index would put the arrays in local memory)
+      const int64_t cyt = t ? cy[1] : cy[0];
+      double sgy_c = 1.0;  // mirror signs (half_generic): per flipped axis
+      if (KIND == PRE && fyt) sgy_c = comp != 1 ? -1.0 : 1.0;  // (-1)^order, and -1 for the
+#pragma unroll                                                   // tangential velocity
+      for (int b = 0; b < n1; ++b) {
+        double lr[n], out[n];
+        const double sgy = (KIND == PRE && fyt && (b & 1)) ? -sgy_c : sgy_c;
 #pragma unroll
-    for (int side_y = 0; side_y < 2; ++side_y) {
-      const int b = side_y == 0 ? t : MM - t;
-      const int col = side_y == 0 ? rl : rh;
-      double lr[n], out[n];
+        for (int sx = 0; sx < 2; ++sx) {
+          const double* base = src + cyt + cx[sx];
+          double sgx = 1.0;
+          if (KIND == PRE && fx[sx]) sgx = comp != 0 ? -1.0 : 1.0;
 #pragma unroll
-      for (int sx = 0; sx < 2; ++sx) {
-        const double* base = src + cy[side_y] + cx[sx];
-        // mirror signs (half_generic): per flipped axis (-1)^order, and -1 for
-        // the velocity component tangential to that wall
-        double sgx = 1.0;
-        if (KIND == PRE && fx[sx]) sgx = comp != 0 ? -1.0 : 1.0;
-        double sgy = 1.0;
-        if (KIND == PRE && fy[side_y]) sgy = ((b & 1) ? -1.0 : 1.0) * (comp != 1 ? -1.0 : 1.0);
-#pragma unroll
-        for (int a = 0; a < n1; ++a) {
-          const double sa = (KIND == PRE && fx[sx] && (a & 1)) ? -sgx : sgx;
-          lr[sx * n1 + a] = sa * sgy * __ldg(base + (a * n1 + b) * P.s_coef);
+          for (int a = 0; a < n1; ++a) {
+            const double sa = (KIND == PRE && fx[sx] && (a & 1)) ? -sgx : sgx;
+            lr[sx * n1 + a] = sa * sgy * __ldg(base + (a * n1 + b) * P.s_coef);
+          }
         }
-      }
-      apply_m<MM>(P, lr, out);
+        apply_m<MM>(P, lr, out);
 #pragma unroll
-      for (int r = 0; r < n; ++r) X[r * S::RS + col] = out[r];
+        for (int r = 0; r < n; ++r) X[r * S::RS + t * n1 + b] = out[r];
+      }
     }
     __syncwarp();
-    // y sweep of rows rl, rh
+    // y sweep of the thread's rows
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = h == 0 ? rl : rh;
+    for (int j = 0; j < NJ; ++j) {
       double lr[n], out[n];
+      const double* yr = X + (2 * j + t) * S::RS;
 #pragma unroll
-      for (int c = 0; c < n; ++c) lr[c] = X[r * S::RS + c];
+      for (int c2 = 0; c2 < n; c2 += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(yr + c2);
+        lr[c2] = v.x;
+        lr[c2 + 1] = v.y;
+      }
       apply_m<MM>(P, lr, out);
       if (KIND == VEL || comp == 0) {
 #pragma unroll
-        for (int c = 0; c < n; ++c) Pj[r * S::RS + c] = out[c];
+        for (int c2 = 0; c2 < n; ++c2) acc[j][c2] = out[c2];
       } else {
+        // div V_0, y term: d_y V_y[r][qy] = V_y[r][qy + 1] (qy + 1) / h
 #pragma unroll
-        for (int c = 0; c < n; ++c) vy[h][c] = out[c];
+        for (int c2 = 0; c2 + 1 < n; ++c2)
+          acc[j][c2] = fma(out[c2 + 1], static_cast<double>(c2 + 1) * inv_h, acc[j][c2]);
+      }
+    }
+    if (KIND == PRE && comp == 0) {
+      // div V_0, x term: d_x V_x[r] = V_x[r + 1] (r + 1) / h; row r + 1 is the
+      // partner's acc[j + t] (zero past row n - 1), we send it acc[j + 1 - t];
+      // ascending j keeps every row until it has been sent
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const double f = static_cast<double>(2 * j + t + 1) * inv_h;
+#pragma unroll
+        for (int c2 = 0; c2 < n; ++c2) {
+          const double hi = j + 1 < NJ ? acc[j + 1][c2] : 0.0;
+          const double up = __shfl_xor_sync(FULL, t ? acc[j][c2] : hi, 1);
+          acc[j][c2] = up * f;
+        }
       }
     }
     __syncwarp();
   }
 
-  const double inv_h = P.inv_h;
   const double lap_c = P.av * inv_h * inv_h;
   if constexpr (KIND == PRE) {
-    // X_1 = div V_0 on the rows this thread owns (all n entries)
-    constexpr Regions<MM, PRE> R{};
+    // X_1 = div V_0 -> shared memory (the last y sweep has read X: synced above)
+    constexpr int last1 = RowLim<MM, PRE, 1, 0>::last;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = h == 0 ? rl : rh;
-      if (h == 1 && r > R.last_row(1)) break;
-      double out[n];
-      if (r + 1 < n) {
-        const double f = static_cast<double>(r + 1);
+    for (int j = 0; j < NJ; ++j) {
+      const int r = 2 * j + t;
+      if (r <= last1) {
 #pragma unroll
-        for (int c = 0; c < n; ++c) out[c] = Pj[(r + 1) * S::RS + c] * f;
-      } else {
-#pragma unroll
-        for (int c = 0; c < n; ++c) out[c] = 0.0;
+        for (int c2 = 0; c2 < n; c2 += 2)
+          *reinterpret_cast<double2*>(X + r * S::RS + c2) = make_double2(acc[j][c2], acc[j][c2 + 1]);
       }
-#pragma unroll
-      for (int c = 0; c + 1 < n; ++c) out[c] = fma(vy[h][c + 1], static_cast<double>(c + 1), out[c]);
-#pragma unroll
-      for (int c = 0; c < n; ++c) X[r * S::RS + c] = out[c] * inv_h;
     }
     __syncwarp();
-    pre_levels<MM, 1>(P, A, X, Pj, t, lap_c, tgt[0]);
+    pre_levels<MM, 1>(P, A, X, t, lap_c, acc, tgt[0]);
   } else {
-    vel_levels<MM, 0>(P, A, X, Pj, t, lap_c, inv_h, tgt);
+    vel_levels<MM, 0>(P, A, X, t, lap_c, inv_h, acc, tgt);
   }
 
   // in-place store + finite flag (check_finite, stepper1d.cpp:121-129)
@@ -394,10 +446,14 @@ __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfPa
 #pragma unroll
     for (int c = 0; c < NOUT; ++c)
 #pragma unroll
-      for (int b = 0; b < n1; ++b) {
-        bad |= !isfinite(tgt[c][b]);
-        P.dst[c][tnode + (rl * n1 + b) * P.t_coef] = tgt[c][b];
-      }
+      for (int s = 0; s < NS; ++s)
+        if (2 * s + t <= MM) {
+#pragma unroll
+          for (int b = 0; b < n1; ++b) {
+            bad |= !isfinite(tgt[c][s][b]);
+            P.dst[c][tnode + ((2 * s + t) * n1 + b) * P.t_coef] = tgt[c][s][b];
+          }
+        }
     if (bad && P.step >= 0) atomicMin(P.flag, P.step);
   }
 }
