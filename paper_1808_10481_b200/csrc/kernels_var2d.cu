@@ -351,22 +351,29 @@ __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfPa
   const double inv_h = P.inv_h;
   double acc[NJ][n];  // this thread's rows of the current level
   // ---- reconstruction (reconstruct_cell_2d, interpolation.cpp:77-113) ----
+  const double sgn_t = t ? -1.0 : 1.0;  // (-1)^t
+  double Mt[NJ][n1];                     // this thread's rows of M_L
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int l = 0; l < n1; ++l) Mt[j][l] = t ? P.M[(2 * j + 1) * n + l] : P.M[2 * j * n + l];
 #pragma unroll
   for (int comp = 0; comp < NSRC; ++comp) {
     const double* src = P.src[comp];
-    // x sweep of the stacked columns of y side t (orders b = 0..m) -> X
-    {
-      const int fyt = t ? fy[1] : fy[0];  // (selects: a runtime index would put the arrays in local memory)
-      const int64_t cyt = t ? cy[1] : cy[0];
+    // x sweep in registers: Y[j][col] (row 2j + t) = sum_l M[2j+t][l] u_l with
+    // u_l = L_l + (-1)^{t+l} R_l of the stacked column col = (side y, order b)
+    double Y[NJ][n];
+#pragma unroll
+    for (int sy = 0; sy < 2; ++sy) {
       double sgy_c = 1.0;  // mirror signs (half_generic): per flipped axis
-      if (KIND == PRE && fyt) sgy_c = comp != 1 ? -1.0 : 1.0;  // (-1)^order, and -1 for the
-#pragma unroll                                                   // tangential velocity
+      if (KIND == PRE && fy[sy]) sgy_c = comp != 1 ? -1.0 : 1.0;  // (-1)^order, and -1 for the
+#pragma unroll                                                      // tangential velocity
       for (int b = 0; b < n1; ++b) {
-        double lr[n], out[n];
-        const double sgy = (KIND == PRE && fyt && (b & 1)) ? -sgy_c : sgy_c;
+        const double sgy = (KIND == PRE && fy[sy] && (b & 1)) ? -sgy_c : sgy_c;
+        double lr[n];
 #pragma unroll
         for (int sx = 0; sx < 2; ++sx) {
-          const double* base = src + cyt + cx[sx];
+          const double* base = src + cy[sy] + cx[sx];
           double sgx = 1.0;
           if (KIND == PRE && fx[sx]) sgx = comp != 0 ? -1.0 : 1.0;
 #pragma unroll
@@ -375,24 +382,23 @@ __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfPa
             lr[sx * n1 + a] = sa * sgy * __ldg(base + (a * n1 + b) * P.s_coef);
           }
         }
-        apply_m<MM>(P, lr, out);
+        double u[n1];
 #pragma unroll
-        for (int r = 0; r < n; ++r) X[r * S::RS + t * n1 + b] = out[r];
+        for (int l = 0; l < n1; ++l) u[l] = fma((l & 1) ? -sgn_t : sgn_t, lr[n1 + l], lr[l]);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          double y = 0.0;
+#pragma unroll
+          for (int l = 0; l < n1; ++l) y = fma(Mt[j][l], u[l], y);
+          Y[j][sy * n1 + b] = y;
+        }
       }
     }
-    __syncwarp();
     // y sweep of the thread's rows
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
-      double lr[n], out[n];
-      const double* yr = X + (2 * j + t) * S::RS;
-#pragma unroll
-      for (int c2 = 0; c2 < n; c2 += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(yr + c2);
-        lr[c2] = v.x;
-        lr[c2 + 1] = v.y;
-      }
-      apply_m<MM>(P, lr, out);
+      double out[n];
+      apply_m<MM>(P, Y[j], out);
       if (KIND == VEL || comp == 0) {
 #pragma unroll
         for (int c2 = 0; c2 < n; ++c2) acc[j][c2] = out[c2];
