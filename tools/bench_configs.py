@@ -35,6 +35,12 @@ def timed(g, stream, steps, warm=3):
     return e0.elapsed_time(e1) / steps
 
 
+def kernel_name(d, variable, variant):
+    if variant != 1:
+        return "generic"
+    return "var2d" if variable else f"tiled{d}d"
+
+
 def run(name, d, m, K, boundary=None, variable=False, steps=20):
     stream = torch.cuda.Stream()
     Ks = list(K)
@@ -53,8 +59,13 @@ def run(name, d, m, K, boundary=None, variable=False, steps=20):
     dof = (d + 1) * (m + 1) ** d * math.prod(Ks)
     rate = dof / (ms * 1e-3)
     line = {"config": name, "d": d, "m": m, "K": Ks, "boundary": boundary or [0] * d, "variable_c2": variable,
-            "kernel": "tiled" if g.kernel_variant == 1 else "generic", "ms_per_step": ms,
+            "kernel": kernel_name(d, variable, g.kernel_variant), "ms_per_step": ms,
             "dof_updates_per_s": rate, "hbm_frac_24B": 24 * rate / HBM}
+    if variable:
+        # + the ap jets of both grids (n^d doubles per node, read once per half step)
+        alg = 24 + 2 * (2 * m + 2) ** d * 8 / ((d + 1) * (m + 1) ** d)
+        line["alg_bytes_per_dof"] = alg
+        line["hbm_frac_alg"] = alg * rate / HBM
     print(json.dumps(line), flush=True)
     del g
     torch.cuda.empty_cache()
