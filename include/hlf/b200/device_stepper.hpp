@@ -62,6 +62,10 @@ class DeviceStepper {
     return out;
   }
   void set_coeff(int grid, const std::vector<double>& jets) { check(hlf_set_coeff(s_, grid, jets.data()), s_); }
+  void set_forcing(int grid, const std::vector<double>& table) {
+    check(hlf_set_forcing(s_, grid, table.data()), s_);
+  }
+  void clear_forcing() { check(hlf_clear_forcing(s_), s_); }
   void set_times(double t_p, double t_v, double dt) { check(hlf_set_times(s_, t_p, t_v, dt), s_); }
   void times(double& t_p, double& t_v, double& dt) const { check(hlf_get_times(s_, &t_p, &t_v, &dt), s_); }
   void set_dt(double dt) { check(hlf_set_dt(s_, dt), s_); }

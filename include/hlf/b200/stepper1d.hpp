@@ -20,9 +20,11 @@
 // to the reference.  Coefficient jets are taken from the problem at
 // construction like the reference (stepper1d.cpp:103-110): constant ap/av run
 // the constant-coefficient kernels, a varying ap runs the per-node ap-jet
-// kernels (leapfrog only; av must be constant).  Problems with a forcing
-// provider or a varying av are rejected with ConfigError (the reference's CPU
-// Stepper1d still covers them).
+// kernels (leapfrog only; av must be constant).  A forcing provider
+// (Problem1d::forcing, stepper1d.cpp:113-119) is evaluated on the host at the
+// nodes and times the reference uses and handed to the device per half step
+// (hlf_set_forcing; leapfrog only).  A varying av is rejected with ConfigError
+// (the reference's CPU Stepper1d still covers it).
 #pragma once
 
 #include <cstring>
@@ -46,7 +48,6 @@ class Stepper1d {
     guard.m = m;
     guard.validate();
     if (prob_.n_fields != 2) throw ConfigError("the staggered scheme needs a two-field system");
-    if (prob_.forcing) throw ConfigError("forcing providers are not supported on the device path");
     op_ = build_interp_operator(m);  // the host operator, handed to the device unchanged
     std::vector<double> ap_prim, ap_dual;
     bool ap_const = true, av_const = true;
@@ -103,26 +104,30 @@ class Stepper1d {
     return st;
   }
 
+  // forcing levels: advance_p at (primary x_j, t_v), advance_v at (dual x_j,
+  // t_p) (stepper1d.cpp:152, 162)
   void advance_p(State1d& st) const {
     upload(st);
+    if (prob_.forcing) dev_->set_forcing(HLF_PRIMARY, forcing_table(false, st.t_v));
     guarded([&] { dev_->advance_p(); }, st);
     download(st);
   }
   void advance_v(State1d& st) const {
     upload(st);
+    if (prob_.forcing) dev_->set_forcing(HLF_DUAL, forcing_table(true, st.t_p));
     guarded([&] { dev_->advance_v(); }, st);
     download(st);
   }
   // stepper1d.cpp:168-172: throws InstabilityError(step_index) like check_finite
   void step_system(State1d& st, int step_index) const {
     upload(st);
-    guarded([&] { dev_->step(step_index); }, st);
+    guarded([&] { forced_or_plain_steps(st, 1, step_index); }, st);
     download(st);
   }
   // extension: n steps with the state resident on the device
   void advance_n(State1d& st, int n, int first_step = 0) const {
     upload(st);
-    guarded([&] { dev_->advance_n(n, first_step); }, st);
+    guarded([&] { forced_or_plain_steps(st, n, first_step); }, st);
     download(st);
   }
 
@@ -204,6 +209,7 @@ class Stepper1d {
 
   DeviceStepper& alt(int scheme) const {
     if (!ap_const_) throw ConfigError("the modified / Dual-Hermite device path needs constant coefficients");
+    if (prob_.forcing) throw ConfigError("the modified / Dual-Hermite device path has no forcing");
     if (!alt_dev_[scheme]) {
       hlf_desc d = desc_;
       d.scheme = scheme;
@@ -216,6 +222,35 @@ class Stepper1d {
       }
     }
     return *alt_dev_[scheme];
+  }
+  // forcing_at(x_j, t)(r), r = 0..n-2, at every node of one grid: [K][n-1][n]
+  std::vector<double> forcing_table(bool dual, double t) const {
+    std::vector<double> out(static_cast<size_t>(grid_.K) * (n_ - 1) * n_, 0.0);
+    for (int j = 0; j < grid_.K; ++j) {
+      const double x = dual ? grid_.dual(j) : grid_.primary(j);
+      for (int r = 0; r + 1 < n_; ++r) {
+        const Jet z = prob_.forcing(r, x, t, grid_.h, n_);
+        for (int i = 0; i < n_ && i < static_cast<int>(z.size()); ++i)
+          out[(static_cast<size_t>(j) * (n_ - 1) + r) * n_ + i] = z[i];
+      }
+    }
+    return out;
+  }
+  // n leapfrog steps on the device; with a forcing provider each step gets
+  // its two tables (p at t_v, v at t_p + dt: the reference's t_p after
+  // advance_p) and runs as one hlf_step
+  void forced_or_plain_steps(const State1d& st, int n, int first_step) const {
+    if (!prob_.forcing) {
+      dev_->advance_n(n, first_step);
+      return;
+    }
+    double t_p = st.t_p, t_v = st.t_v, dt = st.dt;
+    for (int i = 0; i < n; ++i) {
+      dev_->set_forcing(HLF_PRIMARY, forcing_table(false, t_v));
+      dev_->set_forcing(HLF_DUAL, forcing_table(true, t_p + dt));
+      dev_->step(first_step + i);
+      dev_->times(t_p, t_v, dt);
+    }
   }
   std::vector<double> flat(const std::vector<Jet>& jets) const {
     const int n1 = m_ + 1;

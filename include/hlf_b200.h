@@ -13,6 +13,7 @@
  *   hlf_set_times/get_times    <- State1d::t_p, t_v, dt         stepper1d.hpp:50
  *   hlf_set_dt                 <- `st.dt = -dt` (time reversal) tests/test_stepper1d.cpp:288
  *   hlf_set_coeff              <- Stepper1d::ap_prim_/ap_dual_  stepper1d.cpp:103-110 (coefficient jets)
+ *   hlf_set_forcing            <- Stepper1d::forcing_at / Problem1d::forcing  stepper1d.cpp:113-119, problem.hpp:27-29
  *   hlf_advance_p              <- Stepper1d::advance_p          stepper1d.hpp:72, stepper1d.cpp:147-156
  *   hlf_advance_v              <- Stepper1d::advance_v          stepper1d.hpp:73, stepper1d.cpp:158-166
  *   hlf_step                   <- Stepper1d::step_system        stepper1d.hpp:74, stepper1d.cpp:168-172
@@ -109,6 +110,17 @@ hlf_status hlf_set_field(hlf_solver* s, int field, const double* host_aos);
 hlf_status hlf_get_field(hlf_solver* s, int field, double* host_aos);
 /* per-node ap jets, (2m+2)^d entries per node (x-major), for grid HLF_PRIMARY / HLF_DUAL */
 hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets);
+/* 1D forcing (ck_recurrence_variable's z, stepper1d.cpp:22-38): the table for
+   the NEXT half step that updates `grid` (HLF_PRIMARY: hlf_advance_p, evaluated
+   by the reference at (primary x_j, t_v); HLF_DUAL: hlf_advance_v, at (dual x_j,
+   t_p after the pressure half step)).  Host AoS [node][r][s], r = 0..2m
+   (levels z(r) of forcing_at), s = 0..2m+1 (the jet), i.e. (2m+1)(2m+2)
+   doubles per node.  Once a table has been set the solver is in forcing mode:
+   every half step needs a fresh table for its grid (HLF_CONFIG_ERROR
+   otherwise, so hlf_advance_n runs at most one step); hlf_clear_forcing leaves
+   forcing mode.  d = 1, leapfrog scheme only. */
+hlf_status hlf_set_forcing(hlf_solver* s, int grid, const double* host_table);
+hlf_status hlf_clear_forcing(hlf_solver* s);
 hlf_status hlf_set_times(hlf_solver* s, double t_p, double t_v, double dt);
 hlf_status hlf_get_times(const hlf_solver* s, double* t_p, double* t_v, double* dt);
 hlf_status hlf_set_dt(hlf_solver* s, double dt);

@@ -78,6 +78,8 @@ def ref_lib():
             getattr(L, f).argtypes = [C.c_void_p, C.c_double]
             getattr(L, f).restype = C.c_double
         L.ref1d_coeff.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp]
+        L.ref1d_forcing.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp]
+        L.ref1d_forcing.restype = None
         L.ref1d_has_forcing.argtypes = [C.c_void_p]
         L.ref1d_has_forcing.restype = C.c_int
         for f in ("ref1d_init_modified", "ref1d_init_dual"):
@@ -223,6 +225,13 @@ class RefStepper1d:
         out = np.zeros(self.K * n)
         self.L.ref1d_coeff(self.h_, which, int(on_dual), _ptr(out))
         return out.reshape(self.K, n)
+
+    def forcing(self, on_dual: bool, t: float) -> np.ndarray:
+        """forcing_at(x_j, t)(r) at every node: [K, 2m+1, 2m+2] (the table of hlf_set_forcing)"""
+        n = 2 * self.m + 2
+        out = np.zeros(self.K * (n - 1) * n)
+        self.L.ref1d_forcing(self.h_, int(on_dual), t, _ptr(out))
+        return out.reshape(self.K, n - 1, n)
 
     def has_forcing(self) -> bool:
         return bool(self.L.ref1d_has_forcing(self.h_))

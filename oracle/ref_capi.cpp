@@ -203,6 +203,26 @@ void ref1d_coeff(void* h, int which, int on_dual, double* out) {
   }
 }
 
+// the forcing levels forcing_at(x, t)(r), r = 0..2m (stepper1d.cpp:113-119),
+// at every node of one grid: out [K][2m+1][2m+2] (zero without a forcing)
+void ref1d_forcing(void* h, int on_dual, double t, double* out) {
+  const Stepper1d& s = *static_cast<Ref1d*>(h)->stepper;
+  const int n = 2 * s.m() + 2;
+  const auto& fz = s.problem().forcing;
+  for (int j = 0; j < s.grid().K; ++j) {
+    const double x = on_dual ? s.grid().dual(j) : s.grid().primary(j);
+    for (int r = 0; r + 1 < n; ++r) {
+      double* o = out + (static_cast<size_t>(j) * (n - 1) + r) * n;
+      if (!fz) {
+        std::memset(o, 0, sizeof(double) * n);
+        continue;
+      }
+      Jet z = fz(r, x, t, s.grid().h, n);
+      for (int i = 0; i < n; ++i) o[i] = i < static_cast<int>(z.size()) ? z[i] : 0.0;
+    }
+  }
+}
+
 int ref1d_has_forcing(void* h) { return static_cast<bool>(static_cast<Ref1d*>(h)->stepper->problem().forcing); }
 
 // Problem2d exact jets at one point (proj/src/problems.cpp:140-199):

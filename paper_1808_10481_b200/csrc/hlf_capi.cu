@@ -42,6 +42,9 @@ struct hlf_solver {
   int layers[4] = {1, 1, 1, 1};
   int64_t plane[4] = {1, 1, 1, 1};
   double* coeff[2] = {nullptr, nullptr};
+  double* force[2] = {nullptr, nullptr};  // 1D forcing tables [(r n + s)][x] per target grid
+  bool force_on = false;
+  bool force_fresh[2] = {false, false};
   int* flag = nullptr;
   int* flag_host = nullptr;
   double* errbuf = nullptr;     // hlf_error_separable accumulator (device) and its host copy
@@ -323,6 +326,14 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
   P.c_layer = s->plane[tf] * s->E;
   P.step = step;
   P.flag = s->flag;
+  const int fg = s->grid_of(tf);
+  if (s->force_on) {
+    if (!s->force_fresh[fg])
+      return fail(s, HLF_CONFIG_ERROR,
+                  "forcing mode: set this half step's table with hlf_set_forcing (or hlf_clear_forcing)");
+    P.force = s->force[fg];
+    P.f_coef = s->plane[tf];
+  }
   if (zhi < 0) zhi = P.tNz;
   if (zlo < 0 || zhi > P.tNz || zlo > zhi || (s->d != 3 && (zlo != 0 || zhi != P.tNz)))
     return fail(s, HLF_INVALID_ARGUMENT, "layer range outside the target field (ranges are 3D only)");
@@ -346,6 +357,7 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
   if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
   s->launches += launched;
   HLF_CUDA(s, cudaGetLastError());
+  if (s->force_on) s->force_fresh[fg] = false;
   return HLF_OK;
 }
 
@@ -488,6 +500,8 @@ void hlf_destroy(hlf_solver* s) {
     if (f) cudaFree(f);
   for (double*& c : s->coeff)
     if (c) cudaFree(c);
+  for (double*& c : s->force)
+    if (c) cudaFree(c);
   if (s->flag) cudaFree(s->flag);
   if (s->flag_host) cudaFreeHost(s->flag_host);
   if (s->errbuf) cudaFree(s->errbuf);
@@ -534,6 +548,33 @@ hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets) {
     HLF_CUDA(s, cudaMalloc(&s->coeff[grid], bytes));
   }
   return transfer(s, s->coeff[grid], N, s->E, plane * s->E, 0, const_cast<double*>(host_jets), true);
+}
+
+hlf_status hlf_set_forcing(hlf_solver* s, int grid, const double* host_table) {
+  if (!s || (grid != HLF_PRIMARY && grid != HLF_DUAL) || !host_table)
+    return fail(s, HLF_INVALID_ARGUMENT, "bad grid or buffer");
+  if (s->d != 1 || s->scheme != HLF_SCHEME_LEAPFROG)
+    return fail(s, HLF_CONFIG_ERROR, "forcing tables are supported for the 1D leapfrog scheme");
+  cudaSetDevice(s->device);
+  const int* N = grid == HLF_PRIMARY ? s->Np : s->Nd;
+  const int per = (s->n - 1) * s->n;
+  if (!s->force[grid]) {
+    const size_t bytes = static_cast<size_t>(s->num_nodes(grid)) * per * sizeof(double);
+    HLF_CUDA(s, cudaMalloc(&s->force[grid], bytes));
+  }
+  const int64_t plane = static_cast<int64_t>(N[0]) * N[1];
+  hlf_status st = transfer(s, s->force[grid], N, per, plane * per, 0, const_cast<double*>(host_table), true);
+  if (st != HLF_OK) return st;
+  s->force_on = true;
+  s->force_fresh[grid] = true;
+  return HLF_OK;
+}
+
+hlf_status hlf_clear_forcing(hlf_solver* s) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  s->force_on = false;
+  s->force_fresh[0] = s->force_fresh[1] = false;
+  return HLF_OK;
 }
 
 hlf_status hlf_set_times(hlf_solver* s, double t_p, double t_v, double dt) {

@@ -279,7 +279,11 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
 // constant, the 2n stacked values, the two n-entry tables and the target jet
 // live in registers, and the kernel streams at memory speed instead of
 // spilling its tables to local memory.
-template <int MM, bool VAR, int KIND>
+//
+// FRC: a forcing table z_r (ck_recurrence_variable's z, stepper1d.cpp:29-32)
+// is added to every P level, so both tables are live at every level and the
+// full coupled recurrence runs: P[r+1] = ap (.) D V[r] + z_r, V[r+1] = av D P[r].
+template <int MM, bool VAR, int KIND, bool FRC = false>
 __global__ void __launch_bounds__(128) half_1d(const __grid_constant__ HalfParams P) {
   constexpr int n1 = MM + 1, n = 2 * MM + 2;
   const int t0 = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -334,7 +338,45 @@ __global__ void __launch_bounds__(128) half_1d(const __grid_constant__ HalfParam
   const double* apj = VAR ? P.coeff + t0 : nullptr;
   // CK recurrence, count = 2m+2 levels (stepper1d.cpp:22-38)
 #pragma unroll
-  for (int r = 0; r + 1 < n; ++r) {
+  for (int r = 0; FRC && r + 1 < n; ++r) {
+    // P[r+1] = ap (.) D V[r] + z_r and V[r+1] = av (.) D P[r] (both from level r)
+    double Pn[n], Vn[n];
+#pragma unroll
+    for (int e = 0; e < n; ++e) {
+      const double dp = e + 1 < n ? div_h(__dmul_rn(Pt[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P) : 0.0;
+      Vn[e] = __dadd_rn(0.0, __dmul_rn(P.av, dp));
+    }
+    double Sd[n];
+#pragma unroll
+    for (int e = 0; e < n; ++e)
+      Sd[e] = e + 1 < n ? div_h(__dmul_rn(Vt[e + 1 < n ? e + 1 : e], static_cast<double>(e + 1)), P) : 0.0;
+#pragma unroll
+    for (int e = 0; e < n; ++e) {
+      double sacc = 0.0;
+      if (VAR) {
+#pragma unroll
+        for (int ei = 0; ei <= e; ++ei) {
+          const double a = __ldg(apj + ei * P.c_coef);
+          if (a != 0.0) sacc = __dadd_rn(sacc, __dmul_rn(a, Sd[e - ei]));
+        }
+      } else {
+        sacc = __dadd_rn(0.0, __dmul_rn(P.ap, Sd[e]));
+      }
+      Pn[e] = __dadd_rn(sacc, __ldg(P.force + t0 + (r * n + e) * P.f_coef));
+    }
+#pragma unroll
+    for (int e = 0; e < n; ++e) {
+      Pt[e] = Pn[e];
+      Vt[e] = Vn[e];
+    }
+    if ((r + 1) & 1) {  // leapfrog_half_update (stepper1d.cpp:54-61)
+      const double w = P.w[r + 1];
+#pragma unroll
+      for (int f = 0; f < n1; ++f) tgt[f] = __dadd_rn(tgt[f], __dmul_rn(w, KIND == VEL ? Vt[f] : Pt[f]));
+    }
+  }
+#pragma unroll
+  for (int r = 0; !FRC && r + 1 < n; ++r) {
     const bool p_live = (KIND == VEL) == (r % 2 == 0);
     if (p_live) {
 #pragma unroll
@@ -389,6 +431,16 @@ int launch_dm(bool variable, HalfKind kind, const HalfParams& p, cudaStream_t st
   const unsigned blocks = static_cast<unsigned>((total + threads - 1) / threads);
   if (blocks == 0) return 0;
   if constexpr (D == 1) {
+    if (p.force) {
+      if (kind == VEL) {
+        if (variable) half_1d<MM, true, VEL, true><<<blocks, threads, 0, st>>>(p);
+        else half_1d<MM, false, VEL, true><<<blocks, threads, 0, st>>>(p);
+      } else {
+        if (variable) half_1d<MM, true, PRE, true><<<blocks, threads, 0, st>>>(p);
+        else half_1d<MM, false, PRE, true><<<blocks, threads, 0, st>>>(p);
+      }
+      return 1;
+    }
     if (kind == VEL) {
       if (variable) half_1d<MM, true, VEL><<<blocks, threads, 0, st>>>(p);
       else half_1d<MM, false, VEL><<<blocks, threads, 0, st>>>(p);

@@ -281,6 +281,18 @@ class Stepper:
             raise ValueError("coefficient buffer has the wrong size")
         self._c(self._L.hlf_set_coeff(self._h, grid, a.ctypes.data))
 
+    def set_forcing(self, grid: int, table: np.ndarray):
+        """1D forcing jets z_r (r = 0..2m, each 2m+2 long) at every node of
+        `grid` for the next half step updating that grid (hlf_set_forcing:
+        PRIMARY -> advance_p at t_v, DUAL -> advance_v at t_p)."""
+        a = np.ascontiguousarray(table, dtype=np.float64)
+        if a.size != self.num_nodes(grid) * (self.n - 1) * self.n:
+            raise ValueError("forcing table has the wrong size")
+        self._c(self._L.hlf_set_forcing(self._h, grid, a.ctypes.data))
+
+    def clear_forcing(self):
+        self._c(self._L.hlf_clear_forcing(self._h))
+
     def set_times(self, t_p: float, t_v: float, dt: float):
         self._c(self._L.hlf_set_times(self._h, t_p, t_v, dt))
 

@@ -187,9 +187,28 @@ TEST_CASE("standing wave convergence, Hermite-leapfrog") {
   CHECK(std::abs(fit.rate - 6.00) < 0.3);
 }
 
+TEST_CASE("variable speed convergence with forcing, Hermite-leapfrog") {
+  // tests/test_stepper1d.cpp:341-353 with the device stepper: c^2(x) jets and
+  // the forcing provider of variable_speed_problem (problems.cpp:37-61)
+  Problem1d prob = variable_speed_problem();
+  const double T = 3.2, cfl = 0.9;
+  std::vector<int> Ks = {10, 20, 40, 80};
+  std::vector<double> expect = {5.3628e-06, 8.0000e-08, 1.2426e-09, 1.9781e-11};
+  std::vector<double> hs, es;
+  for (size_t i = 0; i < Ks.size(); ++i) {
+    const double e = leapfrog_l2(prob, 2, cfl, Ks[i], T);
+    CHECK(e == doctest::Approx(expect[i]).epsilon(0.02));
+    hs.push_back(2.0 * pi / Ks[i]);
+    es.push_back(e);
+  }
+  RateFit fit = convergence_rate(hs, es);
+  CHECK(std::abs(fit.rate - 6.02) < 0.3);
+}
+
 TEST_CASE("device matches the reference stepper state, constant and variable ap") {
-  for (int variant = 0; variant < 2; ++variant) {
-    Problem1d prob = variant == 0 ? standing_wave_problem() : variable_unforced_problem();
+  for (int variant = 0; variant < 3; ++variant) {
+    Problem1d prob = variant == 0 ? standing_wave_problem()
+                     : variant == 1 ? variable_unforced_problem() : variable_speed_problem();
     for (int m = 0; m <= 5; ++m) {
       Grid1d g = Grid1d::over(prob.x_min, prob.x_max, 32);
       Stepper1d ref(prob, g, m);
@@ -237,7 +256,6 @@ TEST_CASE("discrete invariants hold across steps and orders") {
 
 TEST_CASE("unsupported problem features are configuration errors") {
   Grid1d g = Grid1d::over(0.0, 2.0 * pi, 16);
-  CHECK_THROWS_AS(DeviceStepper1d(variable_speed_problem(), g, 2), ConfigError);  // forcing
   CHECK_THROWS_AS(DeviceStepper1d(standing_wave_problem(), g, 9), ConfigError);   // m cap
   Problem1d adv = advection_problem();
   CHECK_THROWS_AS(DeviceStepper1d(adv, g, 2), ConfigError);                       // one field

@@ -258,6 +258,81 @@ def test_1d_variable_coefficients_vs_compiled_reference():
     assert g.times() == t1
 
 
+def forced_run(r, g, steps):
+    """advance the device solver with the reference problem's forcing tables:
+    advance_p at (primary x_j, t_v), advance_v at (dual x_j, t_p after the
+    pressure half step), as Stepper1d::advance_p/v (stepper1d.cpp:147-166)"""
+    for _ in range(steps):
+        _, t_v, _ = g.times()
+        g.set_forcing(H.PRIMARY, r.forcing(False, t_v))
+        g.advance_p()
+        t_p, _, _ = g.times()
+        g.set_forcing(H.DUAL, r.forcing(True, t_p))
+        g.advance_v()
+
+
+def forced_pair(m, K, dt):
+    r = O.RefStepper1d("variable-speed", m, K)
+    assert r.has_forcing()
+    r.init_leapfrog(dt)
+    p0, v0, t0 = r.get()
+    g = H.Stepper(H.Grid1d.over(r.x_min, r.x_max, K), m, variable_ap=True, av=-1.0)
+    g.set_coeff(0, r.coeff(0, False))
+    g.set_coeff(1, r.coeff(0, True))
+    g.set_field(0, p0)
+    g.set_field(1, v0)
+    g.set_times(*t0)
+    return r, g
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_1d_forcing_bit_identical_to_compiled_reference(m):
+    # variable_speed_problem (problems.cpp:37-61): c^2(x) jets AND a forcing
+    # provider; the faithful 1D kernel with the forcing tables runs the full
+    # coupled recurrence and must reproduce the reference bit for bit
+    if not O.ref_available():
+        pytest.skip("compiled reference not present")
+    K = 32
+    r, g = forced_pair(m, K, 0.9 * (2 * math.pi / K) / math.sqrt(1.5))
+    forced_run(r, g, 30)
+    assert r.steps(30) == -1
+    p1, v1, t1 = r.get()
+    assert np.array_equal(g.get_field(0), p1) and np.array_equal(g.get_field(1), v1)
+    assert g.times() == t1
+
+
+def test_1d_forcing_golden_convergence():
+    # tests/test_stepper1d.cpp:341-353: variable speed, Hermite-leapfrog m = 2,
+    # T = 3.2, cfl 0.9, L2(p) at K = 10/20/40/80 within 2 % of the pinned values
+    if not O.ref_available():
+        pytest.skip("compiled reference not present")
+    m, T, cfl = 2, 3.2, 0.9
+    expect = [5.3628e-06, 8.0000e-08, 1.2426e-09, 1.9781e-11]
+    for K, e_ref in zip([10, 20, 40, 80], expect):
+        h = 2 * math.pi / K
+        n = math.ceil(T / (cfl * h / math.sqrt(1.5)))  # step_count (config.cpp:34-38)
+        r, g = forced_pair(m, K, T / n)
+        forced_run(r, g, n)
+        r.set(g.get_field(0), g.get_field(1), g.times())
+        assert r.l2_p() == pytest.approx(e_ref, rel=0.02), (K, r.l2_p())
+
+
+def test_forcing_mode_needs_a_table_per_half_step():
+    if not O.ref_available():
+        pytest.skip("compiled reference not present")
+    r, g = forced_pair(2, 16, 0.01)
+    forced_run(r, g, 1)
+    with pytest.raises(H.ConfigError):
+        g.advance_p()  # no fresh table
+    with pytest.raises(H.ConfigError):
+        g.advance_n(2)
+    g.clear_forcing()
+    g.advance_n(2)
+    g2 = H.Stepper(H.Grid([-1.0] * 2, 0.2, (10, 10)), 2)
+    with pytest.raises(H.ConfigError):
+        g2.set_forcing(H.PRIMARY, np.zeros((100, 5, 6)))
+
+
 @pytest.mark.parametrize("d", [1, 2, 3])
 def test_time_reversal(d):
     # tests/test_stepper1d.cpp:276-299, in d dimensions
