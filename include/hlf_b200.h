@@ -13,6 +13,7 @@
  *   hlf_set_times/get_times    <- State1d::t_p, t_v, dt         stepper1d.hpp:50
  *   hlf_set_dt                 <- `st.dt = -dt` (time reversal) tests/test_stepper1d.cpp:288
  *   hlf_set_coeff              <- Stepper1d::ap_prim_/ap_dual_  stepper1d.cpp:103-110 (coefficient jets)
+ *   hlf_l2_error_separable     <- l2_error_1d / l2_error_2d      analysis.cpp:241-285 (on the device)
  *   hlf_set_forcing            <- Stepper1d::forcing_at / Problem1d::forcing  stepper1d.cpp:113-119, problem.hpp:27-29
  *   hlf_advance_p              <- Stepper1d::advance_p          stepper1d.hpp:72, stepper1d.cpp:147-156
  *   hlf_advance_v              <- Stepper1d::advance_v          stepper1d.hpp:73, stepper1d.cpp:158-166
@@ -169,6 +170,14 @@ hlf_status hlf_zero_field(hlf_solver* s, int field);
    Synchronous; no state download (convergence sweeps stay on the device). */
 hlf_status hlf_error_separable(hlf_solver* s, int field, double amp, const double* w, const double* phase,
                                double* rms_value, double* max_jet);
+/* Gauss-quadrature L2 error of `field` against amp prod_ax sin(w[ax] x_ax +
+   phase[ax]): the device counterpart of l2_error_1d / l2_error_2d
+   (analysis.cpp:241-285) in d = 1..3 -- cells centred on the other grid's
+   nodes, the cell's Hermite interpolant (reconstruct_cell_*) evaluated at the
+   (2m+2)-point Gauss rule per axis.  Dual-grid fields need periodic axes (the
+   reference clips wall cells); no z slabs. */
+hlf_status hlf_l2_error_separable(hlf_solver* s, int field, double amp, const double* w, const double* phase,
+                                  double* l2);
 
 /* --- z-slab halos (multi-GPU; z_slab = 1) -------------------------------- */
 /* The velocity half step reads p layer Kz (the next rank's layer 0); the

@@ -843,6 +843,78 @@ hlf_status hlf_error_separable(hlf_solver* s, int field, double amp, const doubl
   return HLF_OK;
 }
 
+// n-point Gauss-Legendre rule on [-1, 1] (Newton on P_n; gauss_rule,
+// analysis.cpp:15-33, takes the same nodes from GSL)
+static void gauss_legendre(int n, double* x, double* w) {
+  const double pi = 3.141592653589793238462643383279502884;
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(pi * (i + 0.75) / (n + 0.5)), dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= n; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (n == 1) p0 = 1.0;
+      dp = n * (z * p1 - p0) / (z * z - 1.0);
+      const double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    x[n - 1 - i] = z;
+    w[n - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+hlf_status hlf_l2_error_separable(hlf_solver* s, int field, double amp, const double* w, const double* phase,
+                                  double* l2) {
+  if (!s || !valid_field(s, field) || !w || !phase || !l2) return fail(s, HLF_INVALID_ARGUMENT, "bad argument");
+  const int grid = s->grid_of(field);
+  if (s->z_slab) return fail(s, HLF_CONFIG_ERROR, "the Gauss L2 accessor runs on whole (non-slab) domains");
+  for (int ax = 0; ax < s->d; ++ax)
+    if (grid == HLF_DUAL && s->bnd[ax] != HLF_PERIODIC)
+      return fail(s, HLF_CONFIG_ERROR,
+                  "the Gauss L2 of a dual-grid field needs periodic axes (wall cells are clipped)");
+  if (s->d == 3 && s->m > 4) return fail(s, HLF_CONFIG_ERROR, "3D: m <= 4");
+  cudaSetDevice(s->device);
+  if (!s->errbuf) {
+    HLF_CUDA(s, cudaMalloc(&s->errbuf, 2 * sizeof(double)));
+    HLF_CUDA(s, cudaMallocHost(&s->errbuf_host, 2 * sizeof(double)));
+  }
+  hlfk::L2Params P;
+  std::memset(&P, 0, sizeof(P));
+  std::memcpy(P.M, s->M.data(), sizeof(double) * s->M.size());
+  gauss_legendre(s->n, P.gx, P.gw);
+  P.src = s->field[field];
+  P.layer = s->layer_stride(field);
+  P.coef = s->plane[field];
+  P.zoff = s->zoff(field);
+  P.Nx = s->nodes_of(field)[0];
+  P.shift = grid == HLF_PRIMARY ? 0 : 1;
+  P.h = s->h;
+  P.n = s->n;
+  P.n1 = s->n1;
+  P.d = s->d;
+  P.amp = amp;
+  P.out = s->errbuf;
+  for (int ax = 0; ax < 3; ++ax) {
+    const bool used = ax < s->d;
+    P.cells[ax] = used ? s->K[ax] : 1;
+    P.wrap[ax] = used && s->bnd[ax] == HLF_PERIODIC;
+    P.xc0[ax] = used ? s->x_min[ax] + (grid == HLF_PRIMARY ? 0.5 * s->h : 0.0) : 0.0;
+    P.w[ax] = used ? w[ax] : 0.0;
+    P.phase[ax] = used ? phase[ax] : 0.0;
+  }
+  HLF_CUDA(s, cudaMemsetAsync(s->errbuf, 0, sizeof(double), s->stream));
+  s->launches += hlfk::launch_l2(P, s->stream);
+  HLF_CUDA(s, cudaGetLastError());
+  HLF_CUDA(s, cudaMemcpyAsync(s->errbuf_host, s->errbuf, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+  *l2 = std::sqrt(s->errbuf_host[0]);
+  return HLF_OK;
+}
+
 hlf_status hlf_zero_field(hlf_solver* s, int field) {
   if (!s || !valid_field(s, field)) return fail(s, HLF_INVALID_ARGUMENT, "bad field");
   cudaSetDevice(s->device);

@@ -60,6 +60,24 @@ struct FillParams {
   double* err;                  // launch_error: [sum of squared value errors, max |jet error|]
 };
 
+// Gauss-quadrature L2 error of one field against amp prod sin(w x + phase)
+struct L2Params {
+  double M[kMaxN * kMaxN];
+  double gx[kMaxN], gw[kMaxN];  // n-point Gauss-Legendre rule on [-1, 1]
+  const double* src;            // field base (layer 0 of the allocation)
+  int64_t layer, coef;
+  int zoff;
+  int Nx;                       // field nodes along x (row stride)
+  int cells[3];                 // cells per axis (1 for unused axes)
+  int wrap[3];                  // periodic axis
+  int shift;                    // 0: corners j, j+1 (primary field); 1: j-1, j (dual field)
+  double xc0[3];                // centre of cell 0 per axis
+  double h;
+  int n, n1, d;
+  double amp, w[3], phase[3];
+  double* out;                  // += sum of w (value - exact)^2 (h/2)^d
+};
+
 // 1D alternative schemes of the reference Stepper1d (periodic, constant
 // ap / av): the modified Hermite-leapfrog half pass (step_modified,
 // stepper1d.cpp:191-232) and the two passes of the classic two-half-step
@@ -93,6 +111,7 @@ bool tiled2d_supported(int m);
 int launch_half_var2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
 bool var2d_supported(int m);
 int launch_fill(const FillParams& p, cudaStream_t st);
+int launch_l2(const L2Params& p, cudaStream_t st);
 // field - amp prod sin_jet -> err[0] += sum of squared value errors, err[1] = max |jet error|
 int launch_error(const FillParams& p, cudaStream_t st);
 // z ghost mirror for the dual family: dst layer = sign * (-1)^{c_z} src layer

@@ -387,6 +387,15 @@ class Stepper:
         self._c(self._L.hlf_error_separable(self._h, f, amp, w3, p3, C.byref(rms), C.byref(mx)))
         return rms.value, mx.value
 
+    def l2_error_separable(self, f: int, amp: float, w: Sequence[float], phase: Sequence[float]) -> float:
+        """Gauss-quadrature L2 error of field f against amp * prod sin(w x +
+        phase) (l2_error_1d/2d, analysis.cpp:241-285), computed on the device."""
+        w3 = (C.c_double * 3)(*(list(w) + [0.0] * (3 - len(w))))
+        p3 = (C.c_double * 3)(*(list(phase) + [0.0] * (3 - len(phase))))
+        out = C.c_double()
+        self._c(self._L.hlf_l2_error_separable(self._h, f, amp, w3, p3, C.byref(out)))
+        return out.value
+
     def zero_field(self, f: int):
         self._c(self._L.hlf_zero_field(self._h, f))
 

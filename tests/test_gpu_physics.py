@@ -151,3 +151,101 @@ def test_error_accessor_matches_host(d, m):
         diff = got - ex
         assert rms == pytest.approx(math.sqrt((diff[:, 0] ** 2).mean()), rel=1e-12, abs=1e-300)
         assert mx == pytest.approx(np.abs(diff).max(), rel=1e-12, abs=1e-300)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_gauss_l2_matches_reference_l2_error_1d(have_ref, m):
+    # hlf_l2_error_separable vs the compiled reference's l2_error_1d
+    # (analysis.cpp:241-256) on its own standing-wave state: p on the primary
+    # grid (jets_on_primary) and v on the dual grid
+    if not have_ref:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    K = 12
+    r = O.RefStepper1d("standing-wave", m, K)
+    r.init_leapfrog(0.5 * r.h)
+    assert r.steps(7) == -1
+    p, v, (t_p, t_v, dt) = r.get()
+    g = H.Stepper(H.Grid1d.over(r.x_min, r.x_max, K), m)
+    g.set_field(0, p)
+    g.set_field(1, v)
+    w = 2 * math.pi
+    e_p = g.l2_error_separable(0, math.cos(w * t_p), [w], [0.0])
+    e_v = g.l2_error_separable(1, -math.sin(w * t_v), [w], [math.pi / 2])
+    assert e_p == pytest.approx(r.l2_p(), rel=1e-9)
+    assert e_v == pytest.approx(r.l2_v(), rel=1e-9)
+
+
+def l2_numpy(g, f, amp, w, phase):
+    """the same Gauss-quadrature L2 restated in numpy from a downloaded field"""
+    d, m, n, n1 = g.dim, g.m, g.n, g.n1
+    M = H.build_interp_operator(m).M.reshape(n, n)
+    gx, gw = np.polynomial.legendre.leggauss(n)
+    primary = f == 0
+    K = list(g.grid.K)
+    bnd = list(g.boundary)
+    N = [k + 1 if (primary and b == 1) else k for k, b in zip(K, bnd)]
+    jets = g.get_field(f).reshape(N + [n1] * d)  # host nodes are x-major (x slowest): [x][y][z][orders]
+    Vm = (0.5 * gx[:, None]) ** np.arange(n)[None, :]
+    total = 0.0
+    h = g.grid.h
+    for c in np.ndindex(*K):
+        S = np.zeros((n,) * d)
+        for side in np.ndindex(*([2] * d)):
+            node = []
+            for ax in range(d):
+                q = c[ax] + side[ax] - (0 if primary else 1)
+                node.append(q % K[ax] if bnd[ax] == 0 else q)
+            sl = tuple(slice(s * n1, s * n1 + n1) for s in side)
+            S[sl] = jets[tuple(node)]
+        for ax in range(d):
+            S = np.moveaxis(np.tensordot(M, S, axes=([1], [ax])), 0, ax)
+        V = S
+        for ax in range(d):
+            V = np.moveaxis(np.tensordot(Vm, V, axes=([1], [ax])), 0, ax)
+        ex = amp * np.ones((n,) * d)
+        wt = np.ones((n,) * d)
+        for ax in range(d):
+            xc = g.grid.x_min[ax] + (c[ax] + (0.5 if primary else 0.0)) * h
+            shape = [1] * d
+            shape[ax] = n
+            ex = ex * np.sin(w[ax] * (xc + 0.5 * h * gx) + phase[ax]).reshape(shape)
+            wt = wt * (gw * 0.5 * h).reshape(shape)
+        total += float((wt * (V - ex) ** 2).sum())
+    return math.sqrt(total)
+
+
+@pytest.mark.parametrize("d,m,boundary,f", [(2, 2, [0, 0], 0), (2, 3, [1, 1], 0), (2, 1, [0, 0], 2),
+                                            (3, 2, [0, 0, 0], 3), (3, 1, [1, 0, 1], 0)])
+def test_gauss_l2_matches_numpy_restatement(d, m, boundary, f):
+    K = [6, 5] if d == 2 else [4, 4, 3]
+    g = H.Stepper(H.Grid([-1.0] * d, 2.0 / K[0], tuple(K)), m, boundary=boundary)
+    rng = np.random.default_rng(3 + d + m)
+    a = rng.standard_normal((g.field_nodes(f), g.F)) * 0.6 ** np.arange(g.F)
+    g.set_field(f, a)
+    w = [math.pi, 2.0, 1.5][:d]
+    ph = [0.3, -0.2, 0.1][:d]
+    got = g.l2_error_separable(f, 0.7, w, ph)
+    assert got == pytest.approx(l2_numpy(g, f, 0.7, w, ph), rel=1e-11)
+
+
+def test_gauss_l2_converges_on_the_paper_mode():
+    # 2D acoustics mode: the device L2 of p at T falls at the paper's rate
+    # (PAPER.md:1098, m = 2: 6.01)
+    es = []
+    for K in (16, 32):
+        d, m, T, cfl = 2, 2, 0.5, 0.9
+        h = 2.0 / K
+        n = math.ceil(T / (cfl * h / math.sqrt(d)))
+        dt = T / n
+        g = H.Stepper(H.Grid([-1.0] * d, h, (K,) * d), m)
+        pi = math.pi
+        wt = math.sqrt(d) * pi
+        g.fill_separable(0, 1.0, [pi] * d, [0.0] * d)
+        amp = -pi / wt * math.sin(wt * dt / 2)
+        for c in range(1, d + 1):
+            g.fill_separable(c, amp, [pi] * d, [pi / 2 if a == c - 1 else 0.0 for a in range(d)])
+        g.set_times(0.0, dt / 2, dt)
+        g.advance_n(n)
+        es.append(g.l2_error_separable(0, math.cos(wt * T), [pi] * d, [0.0] * d))
+    rate = math.log2(es[0] / es[1])
+    assert abs(rate - 6.01) < 0.8, (rate, es)
