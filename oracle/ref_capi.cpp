@@ -226,7 +226,7 @@ void ref1d_forcing(void* h, int on_dual, double t, double* out) {
 int ref1d_has_forcing(void* h) { return static_cast<bool>(static_cast<Ref1d*>(h)->stepper->problem().forcing); }
 
 // Problem2d exact jets at one point (proj/src/problems.cpp:140-199):
-// name = acoustics-periodic | acoustics-reflective | gaussian-pulse
+// name = acoustics-periodic | acoustics-reflective | gaussian-pulse | maxwell-tm
 int ref2d_exact(const char* name, int f, double x, double y, double t, double h, int n,
                 double* out) {
   const std::string s(name);
@@ -234,6 +234,7 @@ int ref2d_exact(const char* name, int f, double x, double y, double t, double h,
   if (s == "acoustics-periodic") p = acoustics_mode_problem(Boundary::periodic);
   else if (s == "acoustics-reflective") p = acoustics_mode_problem(Boundary::reflective);
   else if (s == "gaussian-pulse") p = gaussian_pulse_problem();
+  else if (s == "maxwell-tm") p = maxwell_cavity_problem();
   else return 1;
   TensorJet tj = p.exact(f, x, y, t, h, n);
   std::memcpy(out, tj.a.data(), sizeof(double) * tj.a.size());

@@ -5,6 +5,6 @@ C-ABI in include/hlf_b200.h); this package is its host-side mirror of the
 reference's solver interface (proj/include/hlf)."""
 from .solver import (  # noqa: F401
     DUAL, PERIODIC, PRIMARY, REFLECTIVE, ConfigError, CudaError, Grid, Grid1d, Grid2d, Grid3d,
-    InstabilityError, InterpOperator, SchemeConfig, Stepper, Stepper1d, Stepper2d, Stepper3d,
+    InstabilityError, InterpOperator, MaxwellTM2d, SchemeConfig, Stepper, Stepper1d, Stepper2d, Stepper3d,
     SCHEME_DUAL_HERMITE, SCHEME_LEAPFROG, SCHEME_MODIFIED, build_interp_operator, step_count,
 )

@@ -429,3 +429,35 @@ def Stepper2d(grid: Grid, m: int, **kw) -> Stepper:
 
 def Stepper3d(grid: Grid, m: int, **kw) -> Stepper:
     return Stepper(grid, m, **kw)
+
+
+class MaxwellTM2d:
+    """2D Maxwell TM system of the reference's problem catalog (problem.hpp:34-37,
+    maxwell_cavity_problem, problems.cpp:162-183):
+        dEz/dt = dHy/dx - dHx/dy,  dHx/dt = -dEz/dy,  dHy/dt = dEz/dx,
+    Ez on the primary grid, Hx / Hy on the dual grid, PEC walls by default.
+    With p = Ez, v = -Hy, u = Hx it is exactly the acoustics system the
+    steppers run (dp/dt = -(dv/dx + du/dy), dv/dt = -dp/dx, du/dt = -dp/dy,
+    ap = av = -1), and a PEC wall (Ez = 0, normal H odd) is the reflective
+    wall of the acoustic kernels (p zero on the wall line, tangential velocity
+    odd).  This wrapper only maps the fields; every kernel is the acoustic one."""
+
+    def __init__(self, grid: Grid, m: int, boundary=None, **kw):
+        if grid.dim != 2:
+            raise ConfigError("Maxwell TM is a 2D system")
+        self.stepper = Stepper(grid, m, boundary=boundary if boundary is not None else [REFLECTIVE] * 2,
+                               ap=-1.0, av=-1.0, **kw)
+
+    def set_fields(self, Ez: np.ndarray, Hx: np.ndarray, Hy: np.ndarray):
+        self.stepper.set_field(0, Ez)
+        self.stepper.set_field(1, -np.asarray(Hy, dtype=np.float64))
+        self.stepper.set_field(2, Hx)
+
+    def get_fields(self):
+        """(Ez, Hx, Hy) as [node][coef] jets"""
+        s = self.stepper
+        return s.get_field(0), s.get_field(2), -s.get_field(1)
+
+    def __getattr__(self, name):  # stepping, times, accessors: the acoustic stepper's
+        return getattr(self.stepper, name)
+

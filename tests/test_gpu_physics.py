@@ -249,3 +249,41 @@ def test_gauss_l2_converges_on_the_paper_mode():
         es.append(g.l2_error_separable(0, math.cos(wt * T), [pi] * d, [0.0] * d))
     rate = math.log2(es[0] / es[1])
     assert abs(rate - 6.01) < 0.8, (rate, es)
+
+
+def maxwell_jets(f, K, h, n1, t, dual):
+    N = K if dual else K + 1  # PEC walls: the primary grid carries the wall lines
+    off = 0.5 * h if dual else 0.0
+    out = np.zeros((N * N, n1 * n1))
+    for ix in range(N):
+        for iy in range(N):
+            out[ix * N + iy] = O.ref2d_exact("maxwell-tm", f, -1.0 + off + ix * h, -1.0 + off + iy * h, t, h, n1).ravel()
+    return out
+
+
+def test_maxwell_tm_cavity_converges(have_ref):
+    # maxwell_cavity_problem (problems.cpp:162-183): Ez = sin(8 pi x) sin(8 pi y)
+    # cos(wt t) in a PEC box, run through the acoustic kernels by the field map
+    # of MaxwellTM2d; the nodal Ez jets converge to the reference's exact jets
+    if not have_ref:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    m, T = 3, 0.05
+    errs = []
+    for K in (32, 64):
+        h = 2.0 / K
+        n = math.ceil(T / (0.9 * h / math.sqrt(2)))
+        dt = T / n
+        g = H.MaxwellTM2d(H.Grid([-1.0, -1.0], h, (K, K)), m)
+        assert g.kernel_variant == 1
+        g.set_fields(maxwell_jets(0, K, h, m + 1, 0.0, False), maxwell_jets(1, K, h, m + 1, dt / 2, True),
+                     maxwell_jets(2, K, h, m + 1, dt / 2, True))
+        g.set_times(0.0, dt / 2, dt)
+        g.advance_n(n)
+        Ez, Hx, Hy = g.get_fields()
+        t_p, t_v, _ = g.times()
+        ex = maxwell_jets(0, K, h, m + 1, t_p, False)
+        errs.append(np.abs(Ez[:, 0] - ex[:, 0]).max())
+        exh = maxwell_jets(1, K, h, m + 1, t_v, True)
+        assert np.abs(Hx[:, 0] - exh[:, 0]).max() < 50 * errs[-1] + 1e-12
+    rate = math.log2(errs[0] / errs[1])
+    assert errs[1] < 1e-6 and rate > 5.0, (errs, rate)
