@@ -14,6 +14,7 @@
  *   hlf_set_dt                 <- `st.dt = -dt` (time reversal) tests/test_stepper1d.cpp:288
  *   hlf_set_coeff              <- Stepper1d::ap_prim_/ap_dual_  stepper1d.cpp:103-110 (coefficient jets)
  *   hlf_l2_error_separable     <- l2_error_1d / l2_error_2d      analysis.cpp:241-285 (on the device)
+ *   hlf_energy_1d              <- conserved_q / conserved_r      analysis.cpp:221-239 (on the device)
  *   hlf_set_forcing            <- Stepper1d::forcing_at / Problem1d::forcing  stepper1d.cpp:113-119, problem.hpp:27-29
  *   hlf_advance_p              <- Stepper1d::advance_p          stepper1d.hpp:72, stepper1d.cpp:147-156
  *   hlf_advance_v              <- Stepper1d::advance_v          stepper1d.hpp:73, stepper1d.cpp:158-166
@@ -178,6 +179,11 @@ hlf_status hlf_error_separable(hlf_solver* s, int field, double amp, const doubl
    reference clips wall cells); no z slabs. */
 hlf_status hlf_l2_error_separable(hlf_solver* s, int field, double amp, const double* w, const double* phase,
                                   double* l2);
+/* Discrete energy of the 1D periodic leapfrog on the device: kind 0 =
+   conserved_q(p, v_behind, c, dt) (after hlf_advance_p), kind 1 =
+   conserved_r(v_ahead, p, c, dt) (after hlf_advance_v), analysis.cpp:221-239,
+   with the solver's current fields and dt. */
+hlf_status hlf_energy_1d(hlf_solver* s, int kind, double c, double* energy);
 
 /* --- z-slab halos (multi-GPU; z_slab = 1) -------------------------------- */
 /* The velocity half step reads p layer Kz (the next rank's layer 0); the

@@ -915,6 +915,41 @@ hlf_status hlf_l2_error_separable(hlf_solver* s, int field, double amp, const do
   return HLF_OK;
 }
 
+hlf_status hlf_energy_1d(hlf_solver* s, int kind, double c, double* energy) {
+  if (!s || !energy || (kind != 0 && kind != 1)) return fail(s, HLF_INVALID_ARGUMENT, "bad argument");
+  if (s->d != 1 || s->bnd[0] != HLF_PERIODIC || s->scheme != HLF_SCHEME_LEAPFROG)
+    return fail(s, HLF_CONFIG_ERROR, "the discrete energy is defined for the 1D periodic leapfrog");
+  const double sh = c * s->dt / 2.0;
+  if (!(std::fabs(sh) < 0.5 * s->h)) return fail(s, HLF_CONFIG_ERROR, "|c dt / 2| must be below h / 2");
+  cudaSetDevice(s->device);
+  if (!s->errbuf) {
+    HLF_CUDA(s, cudaMalloc(&s->errbuf, 2 * sizeof(double)));
+    HLF_CUDA(s, cudaMallocHost(&s->errbuf_host, 2 * sizeof(double)));
+  }
+  hlfk::EnergyParams P;
+  std::memset(&P, 0, sizeof(P));
+  std::memcpy(P.M, s->M.data(), sizeof(double) * s->M.size());
+  gauss_legendre(s->n1, P.gx, P.gw);
+  P.f = s->field[kind == 0 ? 0 : 1];
+  P.g = s->field[kind == 0 ? 1 : 0];
+  P.coef = s->plane[0];
+  P.f_primary = kind == 0;
+  P.K = s->K[0];
+  P.n = s->n;
+  P.n1 = s->n1;
+  P.x0 = s->x_min[0];
+  P.h = s->h;
+  P.s = sh;
+  P.out = s->errbuf;
+  HLF_CUDA(s, cudaMemsetAsync(s->errbuf, 0, sizeof(double), s->stream));
+  s->launches += hlfk::launch_energy_1d(P, s->stream);
+  HLF_CUDA(s, cudaGetLastError());
+  HLF_CUDA(s, cudaMemcpyAsync(s->errbuf_host, s->errbuf, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+  *energy = s->errbuf_host[0];
+  return HLF_OK;
+}
+
 hlf_status hlf_zero_field(hlf_solver* s, int field) {
   if (!s || !valid_field(s, field)) return fail(s, HLF_INVALID_ARGUMENT, "bad field");
   cudaSetDevice(s->device);

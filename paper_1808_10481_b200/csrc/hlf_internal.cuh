@@ -78,6 +78,19 @@ struct L2Params {
   double* out;                  // += sum of w (value - exact)^2 (h/2)^d
 };
 
+// 1D discrete energy (conserved_q / conserved_r): f, g = the two fields
+struct EnergyParams {
+  double M[kMaxN * kMaxN];
+  double gx[kMaxN], gw[kMaxN];  // (m+1)-point Gauss-Legendre rule
+  const double* f;              // field whose cells are integrated ([coef][node], stride coef)
+  const double* g;              // the other field (shifted by -+ s)
+  int64_t coef;
+  int f_primary;                // f on the primary grid (conserved_q) or the dual grid (conserved_r)
+  int K, n, n1;
+  double x0, h, s;
+  double* out;
+};
+
 // 1D alternative schemes of the reference Stepper1d (periodic, constant
 // ap / av): the modified Hermite-leapfrog half pass (step_modified,
 // stepper1d.cpp:191-232) and the two passes of the classic two-half-step
@@ -112,6 +125,7 @@ int launch_half_var2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st
 bool var2d_supported(int m);
 int launch_fill(const FillParams& p, cudaStream_t st);
 int launch_l2(const L2Params& p, cudaStream_t st);
+int launch_energy_1d(const EnergyParams& p, cudaStream_t st);
 // field - amp prod sin_jet -> err[0] += sum of squared value errors, err[1] = max |jet error|
 int launch_error(const FillParams& p, cudaStream_t st);
 // z ghost mirror for the dual family: dst layer = sign * (-1)^{c_z} src layer

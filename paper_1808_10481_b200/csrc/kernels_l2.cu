@@ -126,7 +126,84 @@ __global__ void __launch_bounds__(128) l2_cells(const __grid_constant__ L2Params
   if ((threadIdx.x & 31) == 0) atomicAdd(P.out, acc);
 }
 
+// Discrete energy of the 1D leapfrog (conserved_q / conserved_r,
+// analysis.cpp:221-239): E = |f - g(. + s)|^2_{m+1} + |f + g(. - s)|^2_{m+1}
+// with f, g the piecewise Hermite interpolants of the two fields
+// (interpolant_from_primary / _from_dual, analysis.cpp:35-86), s = c dt / 2
+// and |.|_{m+1} the Sobolev seminorm of order m+1 (sobolev_seminorm).  One
+// thread per cell of f: the shifted g has one breakpoint inside it (|s| < h/2),
+// and each part is integrated exactly with the (m+1)-point Gauss rule (the
+// integrand has degree 2m).  The reference's pw_shift / pw_combine split and
+// recenter the same polynomials; this evaluates them in place.
+__device__ double deriv_eval(const double* a, int n, int k, double xi, double inv_hk) {
+  double v = 0.0;
+  for (int i = n - 1; i >= k; --i) {
+    double fac = 1.0;
+    for (int q = 0; q < k; ++q) fac *= static_cast<double>(i - q);
+    v = fma(v, xi, a[i] * fac);
+  }
+  return v * inv_hk;
+}
+
+__device__ void recon_1d(const EnergyParams& P, const double* jets, int l, int r, double* out) {
+  double S[kMaxN];
+  for (int a = 0; a < P.n1; ++a) {
+    S[a] = jets[l + a * P.coef];
+    S[P.n1 + a] = jets[r + a * P.coef];
+  }
+  for (int i = 0; i < P.n; ++i) {
+    double v = 0.0;
+    for (int q = 0; q < P.n; ++q) v = fma(P.M[i * P.n + q], S[q], v);
+    out[i] = v;
+  }
+}
+
+__global__ void __launch_bounds__(128) energy_1d(const __grid_constant__ EnergyParams P) {
+  const int j = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double acc = 0.0;
+  if (j < P.K) {
+    const int K = P.K, n = P.n, k = P.n1;  // seminorm order m + 1
+    const double h = P.h;
+    // f cell: primary-based [x_j, x_j+1] around dual j, or dual-based
+    // [x_j-1/2, x_j+1/2] around primary j; g cells left / right of its middle
+    const double a0 = P.x0 + (P.f_primary ? j * h : (j - 0.5) * h);
+    double fa[kMaxN], gl[kMaxN], gr[kMaxN];
+    if (P.f_primary) recon_1d(P, P.f, j, (j + 1) % K, fa);
+    else recon_1d(P, P.f, (j - 1 + K) % K, j, fa);
+    recon_1d(P, P.g, (j - 1 + K) % K, j, gl);
+    recon_1d(P, P.g, j, (j + 1) % K, gr);
+    double inv_hk = 1.0;
+    for (int q = 0; q < k; ++q) inv_hk /= h;
+    const double cf = a0 + 0.5 * h;
+    for (int sg = 0; sg < 2; ++sg) {
+      const double sigma = sg == 0 ? 1.0 : -1.0;  // f - g(x + s), then f + g(x - s)
+      const double bp = a0 + 0.5 * h - sigma * P.s;
+      for (int part = 0; part < 2; ++part) {
+        const double xl = part == 0 ? a0 : bp, xr = part == 0 ? bp : a0 + h;
+        const double* gc = part == 0 ? gl : gr;
+        const double cg = part == 0 ? a0 : a0 + h;
+        const double half = 0.5 * (xr - xl), mid = 0.5 * (xr + xl);
+        for (int q = 0; q < k; ++q) {
+          const double x = mid + half * P.gx[q];
+          const double df = deriv_eval(fa, n, k, (x - cf) / h, inv_hk);
+          const double dg = deriv_eval(gc, n, k, (x + sigma * P.s - cg) / h, inv_hk);
+          const double v = df - sigma * dg;
+          acc = fma(P.gw[q] * half * v, v, acc);
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(P.out, acc);
+}
+
 }  // namespace
+
+int launch_energy_1d(const EnergyParams& p, cudaStream_t st) {
+  if (p.K <= 0) return 0;
+  energy_1d<<<(p.K + 127) / 128, 128, 0, st>>>(p);
+  return 1;
+}
 
 int launch_l2(const L2Params& p, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(p.cells[0]) * p.cells[1] * p.cells[2];

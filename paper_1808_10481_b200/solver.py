@@ -396,6 +396,13 @@ class Stepper:
         self._c(self._L.hlf_l2_error_separable(self._h, f, amp, w3, p3, C.byref(out)))
         return out.value
 
+    def energy_1d(self, kind: int, c: float = 1.0) -> float:
+        """1D discrete energy on the device: kind 0 = conserved_q (after
+        advance_p), 1 = conserved_r (after advance_v), analysis.cpp:221-239."""
+        out = C.c_double()
+        self._c(self._L.hlf_energy_1d(self._h, kind, c, C.byref(out)))
+        return out.value
+
     def zero_field(self, f: int):
         self._c(self._L.hlf_zero_field(self._h, f))
 

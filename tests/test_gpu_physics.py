@@ -287,3 +287,25 @@ def test_maxwell_tm_cavity_converges(have_ref):
         assert np.abs(Hx[:, 0] - exh[:, 0]).max() < 50 * errs[-1] + 1e-12
     rate = math.log2(errs[0] / errs[1])
     assert errs[1] < 1e-6 and rate > 5.0, (errs, rate)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_device_energy_matches_reference(golden, have_ref, m):
+    # hlf_energy_1d (conserved_q / conserved_r on the device) against the
+    # compiled reference's accessors on the same states (analysis.cpp:221-239)
+    if not have_ref:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    e = golden["energy"][str(m)]
+    K, n1 = e["K"], m + 1
+    g = H.Stepper(H.Grid([-1.0], 2.0 / K, (K,)), m, ap=1.0, av=1.0)
+    g.set_field(0, np.array(e["p0"]).reshape(K, n1))
+    g.set_field(1, np.array(e["v0"]).reshape(K, n1))
+    g.set_times(*e["times0"])
+    r = O.RefStepper1d("random-wave", m, K)
+    for _ in range(10):
+        g.advance_p()
+        r.set(g.get_field(0), g.get_field(1), g.times())
+        assert g.energy_1d(0, 1.0) == pytest.approx(r.conserved_q(1.0), rel=1e-11)
+        g.advance_v()
+        r.set(g.get_field(0), g.get_field(1), g.times())
+        assert g.energy_1d(1, 1.0) == pytest.approx(r.conserved_r(1.0), rel=1e-11)
