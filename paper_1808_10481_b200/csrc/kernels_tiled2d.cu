@@ -33,7 +33,7 @@ constexpr int TXC = 32;
 constexpr int RAWX = TXC + 2;  // 33 source nodes used; 34 keeps TMA rows 16 B multiples
 constexpr int NWARP = 4;
 constexpr int NTHREADS = NWARP * 32;
-constexpr int ZC = 32;  // rows per CTA (32: +14 % at 1024^2 m = 3 over 64, equal at 4096^2)
+constexpr int ZC = 32;  // rows per CTA (32: +14 % at 1024^2 m = 3 over 64, equal at 4096^2); see launch_one
 constexpr int kMaxB2 = 15;  // |b| <= 4 in 2D
 
 struct T2Params {
@@ -48,6 +48,7 @@ struct T2Params {
   int sNx, sNy, tNx, tNy;
   int K[2], bnd[2];
   int pre, comp, step;
+  int zc;                       // target rows per CTA
   int tma, tma_t;                  // tensor maps encoded (raw sources / targets)
   int* flag;
 };
@@ -157,8 +158,8 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int x0 = blockIdx.x * TXC;
-  const int j0 = blockIdx.y * ZC;
-  const int j1 = min(j0 + ZC, P.tNy);
+  const int j0 = blockIdx.y * P.zc;
+  const int j1 = min(j0 + P.zc, P.tNy);
   if (j0 >= j1) return;
   const bool active = x0 + lane < P.tNx;
 
@@ -380,7 +381,13 @@ int launch_one(T2Params T, cudaStream_t st) {
     cudaFuncSetAttribute(tiled2d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     configured = true;
   }
-  dim3 grid((T.tNx + TXC - 1) / TXC, (T.tNy + ZC - 1) / ZC);
+  // rows per CTA: ZC, or shorter chunks when the grid has too few CTAs to
+  // fill the SMs evenly (1024^2: m = 1 +7 % at 8 rows, m = 3 +9 % and m = 4
+  // +11 % at 16, m = 2 equal; 4096^2 is best at 32); HLF_T2_ZC overrides
+  static const int zc_env = std::getenv("HLF_T2_ZC") ? std::atoi(std::getenv("HLF_T2_ZC")) : 0;
+  const int64_t ctas32 = static_cast<int64_t>((T.tNx + TXC - 1) / TXC) * ((T.tNy + ZC - 1) / ZC);
+  T.zc = zc_env > 0 ? zc_env : (ctas32 >= 2048 ? ZC : (MM == 1 ? 8 : (MM == 2 ? ZC : 16)));
+  dim3 grid((T.tNx + TXC - 1) / TXC, (T.tNy + T.zc - 1) / T.zc);
   tiled2d<MM, NT><<<grid, NTHREADS, smem, st>>>(T);
   return 1;
 }
