@@ -51,6 +51,25 @@ struct Idx {
   }
 };
 
+// Entries of CK level k that any later level or the target reads: the target
+// needs q <= m per axis at the odd levels, and each level reads the next one
+// shifted by one unit along one axis (d_c T[q] = T[q + e_c] ...), so level k
+// needs excess(q) = sum_c max(0, q_c - m) <= n - 1 - k.  The set is closed
+// downwards, so the truncated products stay inside it.  Skipping the other
+// entries changes no computed value (bit-identical results).
+template <int D, int MM>
+__device__ __forceinline__ int excess(int e) {
+  constexpr int n = 2 * MM + 2;
+  int x = 0;
+#pragma unroll
+  for (int ax = 0; ax < D; ++ax) {
+    const int q = e % n;
+    e /= n;
+    x += q > MM ? q - MM : 0;
+  }
+  return x;
+}
+
 template <int D, int MM, bool VAR, int KIND>
 __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ HalfParams P) {
   constexpr int n1 = MM + 1, n = 2 * MM + 2;
@@ -184,12 +203,14 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
 #pragma unroll 1
   for (int r = 0; r + 1 < n; ++r) {
     const bool p_live = (KIND == VEL) == (r % 2 == 0);
+    const int keep = n - 2 - r;  // level r + 1 entries with excess <= keep are read later
     if (p_live) {
 #pragma unroll 1
       for (int c = 0; c < D; ++c) {
         const int stride = cpow(n, D - 1 - c);
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
+          if (excess<D, MM>(e) > keep) continue;
           const int qc = (e / stride) % n;
           const double dv = qc + 1 < n ? div_h(__dmul_rn(Pt[e + stride], static_cast<double>(qc + 1)), P) : 0.0;
           Vt[c * E + e] = __dmul_rn(P.av, dv);
@@ -204,6 +225,7 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
         const int stride = cpow(n, D - 1 - c);
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
+          if (excess<D, MM>(e) > keep) continue;
           const int qc = (e / stride) % n;
           const double dv = qc + 1 < n ? div_h(__dmul_rn(Vt[c * E + e + stride], static_cast<double>(qc + 1)), P) : 0.0;
           S[e] = __dadd_rn(S[e], dv);
@@ -216,6 +238,7 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
         // the ascending flat order of the reference's full scan
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
+          if (excess<D, MM>(e) > keep) continue;
           int q[3] = {0, 0, 0};
           Idx<D>::template split<n>(e, q);
           double s = 0.0;
@@ -242,7 +265,8 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
         }
       } else {
 #pragma unroll 1
-        for (int e = 0; e < E; ++e) Pt[e] = __dmul_rn(P.ap, S[e]);
+        for (int e = 0; e < E; ++e)
+          if (excess<D, MM>(e) <= keep) Pt[e] = __dmul_rn(P.ap, S[e]);
       }
     }
     // leapfrog_half_update (stepper1d.cpp:54-61): odd levels of the target's table
