@@ -36,6 +36,8 @@ def timed(g, stream, steps, warm=3):
 
 
 def kernel_name(d, variable, variant):
+    if d == 1:
+        return "faithful1d"  # half_1d: register-resident, bit-identical to the reference
     if variant != 1:
         return "generic"
     return "var2d" if variable else f"tiled{d}d"
