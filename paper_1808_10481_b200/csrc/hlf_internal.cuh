@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace hlfk {
 
 constexpr int kMaxM = 8;                 // SchemeConfig::m_cap (config.hpp:31)
@@ -109,6 +111,18 @@ struct Scheme1dParams {
   int step;
   int* flag;
 };
+
+// The dynamic shared-memory opt-in (cudaFuncSetAttribute) is per device:
+// set it once per kernel and device (devices 0..63), thread-safely.
+template <class Kernel>
+inline void ensure_smem_opt_in(Kernel kernel, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
+    done.fetch_or(bit, std::memory_order_release);
+}
 
 // launchers (return the number of kernels launched)
 int launch_modified_1d(int m, const Scheme1dParams& p, cudaStream_t st);

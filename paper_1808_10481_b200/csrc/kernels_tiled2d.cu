@@ -376,11 +376,8 @@ int launch_one(T2Params T, cudaStream_t st) {
   for (int t = 0; t < NTT && T.tma_t; ++t) T.tma_t = encode_map(&T.tmapT[t], T.dst[t], T.tNx, T.tNy, F, T.t_plane, TXC);
   constexpr int RST = (NT == 3 || MM >= 4) ? 1 : 2;
   const size_t smem = sizeof(double) * (RST * NS * RAWS + 2 * NS * n * n1 * TXC + 2 * NTT * F * TXC) + 128;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tiled2d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    configured = true;
-  }
+  static std::atomic<unsigned long long> configured{0};
+  ensure_smem_opt_in(tiled2d<MM, NT>, static_cast<int>(smem), configured);
   // rows per CTA: ZC, or shorter chunks when the grid has too few CTAs to
   // fill the SMs evenly (1024^2: m = 1 +7 % at 8 rows, m = 3 +9 % and m = 4
   // +11 % at 16, m = 2 equal; 4096^2 is best at 32); HLF_T2_ZC overrides

@@ -633,11 +633,8 @@ int launch_one(TParams T, cudaStream_t st) {
   }
   using G = Cfg<MM>;
   const size_t smem = sizeof(double) * G::template SMEM_DOUBLES<NT> + 128;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tiled3d<MM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    configured = true;
-  }
+  static std::atomic<unsigned long long> configured{0};
+  ensure_smem_opt_in(tiled3d<MM, NT>, static_cast<int>(smem), configured);
   dim3 grid((T.tNx + TXC - 1) / TXC, T.tNy, (T.tNz + ZC - 1) / ZC);
   tiled3d<MM, NT><<<grid, NTHREADS, smem, st>>>(T);
   return 1;

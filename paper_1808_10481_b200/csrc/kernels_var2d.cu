@@ -470,12 +470,9 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(p.tNx) * p.tNy;
   const int64_t blocks = (total + S::CPC - 1) / S::CPC;
   if (blocks > 0x7fffffff) return -2;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(var2d<MM, VEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    cudaFuncSetAttribute(var2d<MM, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    init = true;
-  }
+  static std::atomic<unsigned long long> vel_ok{0}, pre_ok{0};
+  if (kind == VEL) ensure_smem_opt_in(var2d<MM, VEL>, S::SMEM, vel_ok);
+  else ensure_smem_opt_in(var2d<MM, PRE>, S::SMEM, pre_ok);
   if (kind == VEL)
     var2d<MM, VEL><<<static_cast<unsigned>(blocks), NTHREADS, S::SMEM, st>>>(p);
   else
