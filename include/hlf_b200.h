@@ -150,6 +150,10 @@ hlf_status hlf_step(hlf_solver* s, int step_index);
    the first offending step index is reported through HLF_INSTABILITY */
 hlf_status hlf_advance_n(hlf_solver* s, int n, int first_step);
 /* -1 when the state stayed finite, else the first non-finite step index */
+/* hlf_advance_n replays runs of `steps` leapfrog steps as one captured CUDA
+   graph (launch overhead dominates small grids); 0 = launch every kernel
+   directly.  Default 32; used when n >= 2 * steps. */
+hlf_status hlf_set_graph_steps(hlf_solver* s, int steps);
 hlf_status hlf_poll_finite(hlf_solver* s, int* first_bad_step);
 hlf_status hlf_clear_finite(hlf_solver* s);
 hlf_status hlf_synchronize(hlf_solver* s);

@@ -28,6 +28,14 @@ struct hlf_solver {
   double x_min[3] = {0, 0, 0};
   double h = 1.0, ap = -1.0, av = -1.0;
   bool variable = false;
+  // CUDA graph of graph_chunk leapfrog steps, replayed by hlf_advance_n
+  // (small grids are launch bound); rebuilt when dt, the kernel variant or a
+  // kernel pointer (gen) changes
+  int graph_chunk = 32;
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_steps = 0, graph_variant = -1, graph_kernels = 0;
+  double graph_dt = 0.0;
+  uint64_t gen = 1, graph_gen = 0;
   bool m_mirror = true;  // M_R = diag((-1)^r) M_L diag((-1)^l): the fast kernels use M_L only
   bool z_slab = false;
   int scheme = HLF_SCHEME_LEAPFROG;
@@ -478,12 +486,12 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
     e = cudaMemsetAsync(s->field[f], 0, bytes, s->stream);
     if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaMemset(field)"));
   }
-  e = cudaMalloc(&s->flag, sizeof(int));
+  e = cudaMalloc(&s->flag, 2 * sizeof(int));
   if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaMalloc(flag)"));
   e = cudaMallocHost(&s->flag_host, sizeof(int));
   if (e != cudaSuccess) return bail(cuda_fail(s, e, "cudaMallocHost(flag)"));
-  const int big = INT_MAX;
-  e = cudaMemcpyAsync(s->flag, &big, sizeof(int), cudaMemcpyHostToDevice, s->stream);
+  const int init_flag[2] = {INT_MAX, 0};  // [first bad step, graph step base]
+  e = cudaMemcpyAsync(s->flag, init_flag, sizeof(init_flag), cudaMemcpyHostToDevice, s->stream);
   if (e != cudaSuccess) return bail(cuda_fail(s, e, "flag init"));
   e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) return bail(cuda_fail(s, e, "sync"));
@@ -502,6 +510,7 @@ void hlf_destroy(hlf_solver* s) {
     if (c) cudaFree(c);
   for (double*& c : s->force)
     if (c) cudaFree(c);
+  if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
   if (s->flag) cudaFree(s->flag);
   if (s->flag_host) cudaFreeHost(s->flag_host);
   if (s->errbuf) cudaFree(s->errbuf);
@@ -546,6 +555,7 @@ hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets) {
   if (!s->coeff[grid]) {
     const size_t bytes = static_cast<size_t>(s->num_nodes(grid)) * s->E * sizeof(double);
     HLF_CUDA(s, cudaMalloc(&s->coeff[grid], bytes));
+    ++s->gen;
   }
   return transfer(s, s->coeff[grid], N, s->E, plane * s->E, 0, const_cast<double*>(host_jets), true);
 }
@@ -719,6 +729,57 @@ static hlf_status step_async(hlf_solver* s, int step_index) {
   return HLF_OK;
 }
 
+__global__ void set_graph_step_base(int* flag, int base) { flag[1] = base; }
+
+// host time stamps of one step, as step_async / scheme1d_step advance them
+static void advance_times(hlf_solver* s) {
+  s->t_p += s->dt;
+  if (s->scheme == HLF_SCHEME_LEAPFROG) s->t_v += s->dt;
+  else s->t_v = s->scheme == HLF_SCHEME_MODIFIED ? s->t_p + s->dt / 2.0 : s->t_p;
+}
+
+// capture `chunk` steps (step offsets 0..chunk-1) into s->graph_exec; on any
+// capture problem graphs are switched off and the caller launches directly
+static void ensure_graph(hlf_solver* s, int chunk) {
+  if (s->graph_exec && s->graph_steps == chunk && s->graph_dt == s->dt && s->graph_variant == s->variant &&
+      s->graph_gen == s->gen)
+    return;
+  if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
+  s->graph_exec = nullptr;
+  const double t_p = s->t_p, t_v = s->t_v;
+  const int64_t launches = s->launches;
+  hlf_status st = HLF_OK;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    for (int k = 0; k < chunk && st == HLF_OK; ++k) st = step_async(s, k);
+    if (cudaStreamEndCapture(s->stream, &g) != cudaSuccess) st = HLF_CUDA_ERROR;
+  } else {
+    st = HLF_CUDA_ERROR;
+  }
+  s->t_p = t_p;
+  s->t_v = t_v;
+  s->graph_kernels = static_cast<int>(s->launches - launches);
+  s->launches = launches;
+  if (st == HLF_OK && g && cudaGraphInstantiate(&s->graph_exec, g, 0) == cudaSuccess) {
+    s->graph_steps = chunk;
+    s->graph_dt = s->dt;
+    s->graph_variant = s->variant;
+    s->graph_gen = s->gen;
+  } else {
+    s->graph_exec = nullptr;
+    s->graph_chunk = 0;  // fall back to direct launches for this solver
+  }
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+}
+
+hlf_status hlf_set_graph_steps(hlf_solver* s, int steps) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (steps < 0) return fail(s, HLF_INVALID_ARGUMENT, "negative graph chunk");
+  s->graph_chunk = steps;
+  return HLF_OK;
+}
+
 hlf_status hlf_step(hlf_solver* s, int step_index) {
   if (!s) return HLF_INVALID_ARGUMENT;
   cudaSetDevice(s->device);
@@ -734,7 +795,28 @@ hlf_status hlf_advance_n(hlf_solver* s, int n, int first_step) {
   if (!s) return HLF_INVALID_ARGUMENT;
   if (n < 0) return fail(s, HLF_INVALID_ARGUMENT, "negative step count");
   cudaSetDevice(s->device);
-  for (int i = 0; i < n; ++i) {
+  int i = 0;
+  const int chunk = s->graph_chunk;
+  if (chunk > 0 && n >= 2 * chunk && !s->force_on && !s->z_slab) {
+    // the first step runs directly (one-time launch set-up stays out of the
+    // capture), then whole chunks replay the graph with their step base
+    hlf_status st = step_async(s, first_step);
+    if (st != HLF_OK) return st;
+    i = 1;
+    ensure_graph(s, chunk);
+    if (s->graph_exec) {
+      for (; n - i >= chunk; i += chunk) {
+        set_graph_step_base<<<1, 1, 0, s->stream>>>(s->flag, first_step + i);
+        HLF_CUDA(s, cudaGraphLaunch(s->graph_exec, s->stream));
+        for (int k = 0; k < chunk; ++k) advance_times(s);
+        s->launches += s->graph_kernels + 1;
+      }
+      set_graph_step_base<<<1, 1, 0, s->stream>>>(s->flag, 0);
+      s->launches += 1;
+      HLF_CUDA(s, cudaGetLastError());
+    }
+  }
+  for (; i < n; ++i) {
     hlf_status st = step_async(s, first_step + i);
     if (st != HLF_OK) return st;
   }
@@ -995,6 +1077,7 @@ hlf_status hlf_set_kernel_variant(hlf_solver* s, int variant) {
     return fail(s, HLF_CONFIG_ERROR, "tiled kernel not available for this configuration");
   if (variant != 0 && variant != 1) return fail(s, HLF_INVALID_ARGUMENT, "unknown variant");
   s->variant = variant;
+  ++s->gen;
   return HLF_OK;
 }
 

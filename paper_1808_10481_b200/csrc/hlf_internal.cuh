@@ -48,7 +48,7 @@ struct HalfParams {
   int K[3];
   int bnd[3];                   // 0 periodic, 1 reflective (x, y in-kernel; z via ghost layers)
   int step;                     // step index for the finite flag, -1 = do not record
-  int* flag;                    // first non-finite step (atomicMin)
+  int* flag;                    // [first non-finite step (atomicMin), graph step base]
 };
 
 struct FillParams {
@@ -111,6 +111,13 @@ struct Scheme1dParams {
   int step;
   int* flag;
 };
+
+// First non-finite step: flag[0] = min over reports, flag[1] = the step base
+// of a replayed CUDA graph (kernels captured in one carry the step offset
+// within it; 0 for direct launches).  Read only on the failure path.
+__device__ __forceinline__ void report_nonfinite(int* flag, int step) {
+  atomicMin(flag, step + *reinterpret_cast<volatile int*>(flag + 1));
+}
 
 // The dynamic shared-memory opt-in (cudaFuncSetAttribute) is per device:
 // set it once per kernel and device (devices 0..63), thread-safely.

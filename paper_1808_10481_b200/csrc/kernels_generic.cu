@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
       P.dst[c][toff + f * P.t_coef] = nv;
     }
 
-  if (bad && P.step >= 0) atomicMin(P.flag, P.step);
+  if (bad && P.step >= 0) report_nonfinite(P.flag, P.step);
 }
 
 // 1D: the same faithful arithmetic, operation for operation (so results stay
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(128) half_1d(const __grid_constant__ HalfParam
     bad |= !isfinite(tgt[f]);
     P.dst[0][toff + f * P.t_coef] = tgt[f];
   }
-  if (bad && P.step >= 0) atomicMin(P.flag, P.step);
+  if (bad && P.step >= 0) report_nonfinite(P.flag, P.step);
 }
 
 template <int D, int MM>
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(128) modified_1d(const __grid_constant__ Schem
     P.dst_p[j + s2 * P.K] = op[s2];
     P.dst_v[j + s2 * P.K] = ov[s2];
   }
-  if (bad && P.step >= 0) atomicMin(P.flag, P.step);
+  if (bad && P.step >= 0) report_nonfinite(P.flag, P.step);
 }
 
 // one pass of step_dual_hermite: taylor_advance by tau = dt/2 (stepper1d.cpp:63-71, 249-272)
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(128) dual_hermite_1d(const __grid_constant__ S
     P.dst_p[j + s2 * P.K] = op[s2];
     P.dst_v[j + s2 * P.K] = ov[s2];
   }
-  if (PASS == 1 && bad && P.step >= 0) atomicMin(P.flag, P.step);
+  if (PASS == 1 && bad && P.step >= 0) report_nonfinite(P.flag, P.step);
 }
 
 }  // namespace

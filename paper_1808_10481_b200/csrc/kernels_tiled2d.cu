@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
     rob = rnb;
     rnb = tmp;
   }
-  if (bad && active && P.step >= 0) atomicMin(P.flag, P.step);
+  if (bad && active && P.step >= 0) report_nonfinite(P.flag, P.step);
 }
 
 double host_fact(int k) {

@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     ro = rn;
     rn = tmp;
   }
-  if (emax >= 0x7ff00000 && zactive && P.step >= 0) atomicMin(P.flag, P.step);
+  if (emax >= 0x7ff00000 && zactive && P.step >= 0) report_nonfinite(P.flag, P.step);
 }
 
 double host_fact(int k) {

@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfPa
             P.dst[c][tnode + ((2 * s + t) * n1 + b) * P.t_coef] = tgt[c][s][b];
           }
         }
-    if (bad && P.step >= 0) atomicMin(P.flag, P.step);
+    if (bad && P.step >= 0) report_nonfinite(P.flag, P.step);
   }
 }
 

@@ -290,6 +290,10 @@ class Stepper:
             raise ValueError("forcing table has the wrong size")
         self._c(self._L.hlf_set_forcing(self._h, grid, a.ctypes.data))
 
+    def set_graph_steps(self, steps: int):
+        """advance_n replays runs of `steps` steps as one CUDA graph (0: off)"""
+        self._c(self._L.hlf_set_graph_steps(self._h, steps))
+
     def clear_forcing(self):
         self._c(self._L.hlf_clear_forcing(self._h))
 

@@ -525,3 +525,42 @@ def test_parity_2d_tiled_kernel(m, boundary):
     assert g.kernel_variant == 1
     run_both(g, o, 5, 0.3 * g.grid.h)
     compare(g, o, 2)
+
+
+@pytest.mark.parametrize("d,m,K,boundary", [(1, 3, [256], [0]), (2, 2, [40, 33], [1, 0]), (2, 3, [20, 20], [1, 1]),
+                                            (3, 3, [36, 4, 6], [0, 0, 0]), (3, 2, [8, 6, 5], [1, 1, 1])])
+def test_graph_replay_is_bit_identical(d, m, K, boundary):
+    # hlf_advance_n replays chunks of steps as a captured CUDA graph; the
+    # fields, time stamps and launch sequence must equal direct launches
+    runs = []
+    for chunk in (4, 0):
+        g, _ = make_pair(d, m, K, boundary=boundary, seed=31)
+        g.set_graph_steps(chunk)
+        dt = 0.25 * g.grid.h
+        g.set_times(0.0, dt / 2, dt)
+        g.advance_n(23, 5)
+        g.advance_n(9, 28)  # cached graph, new step base
+        runs.append(([g.get_field(f) for f in range(d + 1)], g.times()))
+    (fa, ta), (fb, tb) = runs
+    assert ta == tb
+    for a, b in zip(fa, fb):
+        assert np.array_equal(a, b)
+
+
+def test_graph_replay_reports_the_first_bad_step():
+    # the step index of a blow-up inside a replayed chunk (graph step base)
+    grid = H.Grid1d.over(-1.0, 1.0, 16)
+    p = np.zeros((16, 3))
+    O.add_separable(1, [16], [-1.0], grid.h, 0.0, 3, 1.0, [2 * math.pi], [0.0], p)
+    idx = []
+    for chunk in (0, 4):
+        g = H.Stepper(grid, 2)
+        g.set_graph_steps(chunk)
+        g.set_field(0, p)
+        g.zero_field(1)
+        dt = 2.5 * grid.h
+        g.set_times(0, dt / 2, dt)
+        with pytest.raises(H.InstabilityError) as ei:
+            g.advance_n(5000, 3)
+        idx.append(ei.value.step)
+    assert idx[0] == idx[1] and idx[0] > 3

@@ -24,12 +24,14 @@ HBM = 6551.4e9  # MEASURED_PEAKS.json hbm_gbs
 
 
 def timed(g, stream, steps, warm=3):
-    g.advance_n(warm)
+    # warm-up with the timed step count too: advance_n captures its CUDA graph
+    # (small grids) on the first call with a given chunk and dt
+    g.advance_n(max(warm, steps))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
-    g.advance_n(steps, warm)
+    g.advance_n(steps, max(warm, steps))
     e1.record(stream)
     e1.synchronize()
     return e0.elapsed_time(e1) / steps
