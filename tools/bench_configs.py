@@ -24,14 +24,15 @@ HBM = 6551.4e9  # MEASURED_PEAKS.json hbm_gbs
 
 
 def timed(g, stream, steps, warm=3):
-    # warm-up with the timed step count too: advance_n captures its CUDA graph
-    # (small grids) on the first call with a given chunk and dt
-    g.advance_n(max(warm, steps))
+    # advance_n captures its CUDA graph (runs of >= 64 steps) on the first call
+    # with a given dt: warm up with the timed step count there
+    warm = steps if steps >= 64 else warm
+    g.advance_n(warm)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
-    g.advance_n(steps, max(warm, steps))
+    g.advance_n(steps, warm)
     e1.record(stream)
     e1.synchronize()
     return e0.elapsed_time(e1) / steps
