@@ -215,6 +215,32 @@ __device__ __forceinline__ void ck(int c, int w, const TParams& P, const double 
   else m3_ck(c, w, P, pt, acc);
 }
 
+// merged pressure launch (c < 0): the index shift is in the sweep rows
+template <int MM>
+__device__ __forceinline__ void ck_any(int c, int w, const TParams& P, const double (&pt)[MM + 1][MM + 1][MM + 1],
+                                       double (&acc)[(MM + 2) / 2][(MM + 2) / 2][(MM + 2) / 2]) {
+  if constexpr (MM == 1) {
+    if (c < 0) m1_ck_noshift(w, P, pt, acc); else m1_ck(c, w, P, pt, acc);
+  } else if constexpr (MM == 2) {
+    if (c < 0) m2_ck_noshift(w, P, pt, acc); else m2_ck(c, w, P, pt, acc);
+  } else {
+    ck<MM>(c, w, P, pt, acc);
+  }
+}
+
+// merged XY task (V_x through rows q_x+1, V_y through rows q_y+1)
+template <int MM>
+__device__ __forceinline__ void xy_merged(int px, const TParams& P, const double* rbx, const double* rby,
+                                          double* wb) {
+  if constexpr (MM == 1) {
+    if (px) m1_xy_px1_vxy(P, rbx, rby, wb); else m1_xy_px0_vxy(P, rbx, rby, wb);
+  } else if constexpr (MM == 2) {
+    if (px) m2_xy_px1_vxy(P, rbx, rby, wb); else m2_xy_px0_vxy(P, rbx, rby, wb);
+  } else {
+    if (px) m3_xy_px1_vxy(P, rbx, rby, wb); else m3_xy_px0_vxy(P, rbx, rby, wb);
+  }
+}
+
 // 1/o! for o <= 3 without a dynamically indexed parameter load
 __device__ __forceinline__ double ifact_s(int o) { return o <= 1 ? 1.0 : (o == 2 ? 0.5 : 1.0 / 6.0); }
 
@@ -226,7 +252,6 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   constexpr int NB = G::template NBUF<NT>;
   constexpr bool MX = NT == 2;                // merged V_x + V_y pressure launch
   constexpr int NTT = G::template NTGT<NT>;   // target fields
-  static_assert(!MX || MM == 3, "merged pressure launch is generated for m = 3");
   extern __shared__ __align__(128) double smem_raw[];
   // TMA tensor destinations must be 128 B aligned: align the base explicitly
   // (the launch requests 128 B of slack)
@@ -469,13 +494,15 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       if (k + 1 < k1) issue_raw(k + 2); else cp_async_commit();
     }
 #ifndef HLF_EXP_NOXY
-    if constexpr (MX) {
+    if (MX && warp >= 2 * n1) {
+      // m < 3: fewer (l_z, q_x parity) tasks than warps
+    } else if constexpr (MX) {
       const int lz = warp >> 1;
       double* wb = rn + lz * TXC + lane;
       const double* rbx = rawbuf + lz * 2 * RAWX + lane;
       const double* rby = rbx + G::RAWS;
 #ifndef HLF_XY_RMW
-      if (warp & 1) m3_xy_px1_vxy(P, rbx, rby, wb); else m3_xy_px0_vxy(P, rbx, rby, wb);
+      xy_merged<MM>(warp & 1, P, rbx, rby, wb);
 #else
       if (warp & 1) {
         m3_xy_px1_vx(P, rbx, wb);
@@ -529,7 +556,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
         const double* tp = tgs + (t * F + f0) * TXC + zcell;
 #ifndef HLF_EXP_NOCK
         if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);
-        else ck<MM>(c, warp, P, pt, acc);
+        else ck_any<MM>(c, warp, P, pt, acc);
 #else
         acc[0][0][0] += pt[0][0][0] + pt[3][3][3] + pt[1][2][3];
 #endif
@@ -686,7 +713,9 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.dst[0] = p.dst[0];
   int launched = 0;
   static const bool merge = std::getenv("HLF_NO_MERGE") == nullptr;
-  if constexpr (MM == 3) {
+  {
+    // merged V_x + V_y launch: m = 3 +5.9 %, m = 1 +19.5 %, m = 2 +20 % (the
+    // p read-modify-write of one pressure launch saved)
     if (merge) {
       // V_x and V_y divergence terms in one launch, V_z in a second
       T.comp = -1;

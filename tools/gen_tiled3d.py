@@ -209,14 +209,13 @@ def main():
         for px in range(2):
             parts.append(gen_xy(mm, px))
             parts.append("")
-            if mm == 3:
-                # merged pressure (V_x + V_y) launch: C = (My x Mx^{+1}) V_x + (My^{+1} x Mx) V_y
-                parts.append(gen_xy(mm, px, shx=1, suffix="_vx"))
-                parts.append("")
-                parts.append(gen_xy(mm, px, shy=1, acc=True, suffix="_vy"))
-                parts.append("")
-                parts.append(gen_xy_merged(mm, px))
-                parts.append("")
+            # merged pressure (V_x + V_y) launch: C = (My x Mx^{+1}) V_x + (My^{+1} x Mx) V_y
+            parts.append(gen_xy(mm, px, shx=1, suffix="_vx"))
+            parts.append("")
+            parts.append(gen_xy(mm, px, shy=1, acc=True, suffix="_vy"))
+            parts.append("")
+            parts.append(gen_xy_merged(mm, px))
+            parts.append("")
         for pz in range(2):
             parts.append(gen_z(mm, pz))
             parts.append("")
@@ -247,6 +246,29 @@ def main():
             for k in keys:
                 parts.append(f"    case {k}:")
             parts.append(f"      {fn}(P, pt, acc);")
+            parts.append("      break;")
+        parts.append("    default: break;")
+        parts.append("  }")
+        parts.append("}")
+        parts.append("")
+        # merged pressure launch: the index shift sits in the sweep rows, so the
+        # CK has no shift (c = -1); per class w (deduplicated)
+        ns = {}
+        parts.append(f"__device__ __forceinline__ void m{mm}_ck_noshift(int w, const TParams& P,")
+        parts.append(f"    const double (&pt)[{nh}][{nh}][{nh}], double (&acc)[{jh}][{jh}][{jh}]) {{")
+        parts.append("  switch (w) {")
+        for w in range(8):
+            cls = ((w >> 2) & 1, (w >> 1) & 1, w & 1)
+            outs, stm = ck_body(mm, -1, cls)
+            key = "\n".join(stm)
+            fn = bodies.get(key)
+            if fn is None:
+                fn = ns.get(key)
+            parts.append(f"    case {w}:")
+            if fn is not None:
+                parts.append(f"      {fn}(P, pt, acc);")
+            else:
+                parts.extend("    " + x for x in stm)
             parts.append("      break;")
         parts.append("    default: break;")
         parts.append("  }")
