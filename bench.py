@@ -271,7 +271,7 @@ def main():
                        "m": M, "cells_per_gpu": [NX, NY, nz], "global_cells": list(Kg),
                        "dof_per_step": dof_total, "parallelism": f"z-slab x{world}",
                        "l2": "state (128 GiB per GPU) far larger than L2; no flush needed",
-                       "init": "separable standing mode p = sin(pi x) sin(pi y) sin(pi z), exact jets on device"},
+                       "init": "standing mode of the periodic box, p = cos(wt t) prod sin(2 pi x_a / L_a) (512x512x256, h = 1/256: sin(pi x) sin(pi y) sin(2 pi z)), exact jets on device"},
             "gpu_launches": launches,
             "roofline": roofline,
             "clocks": clk.summary(),

@@ -149,21 +149,23 @@ class SlabStepper:
 
     # ---- data
     def init_mode(self, cfl: float = 0.9, t0: float = 0.0):
-        """Standing mode p = sin(pi x) sin(pi y) sin(pi z) cos(sqrt(3) pi t) on
-        [-1, 1]^3 and its velocity v_c = -(1/sqrt 3) d_c(...) sin(sqrt(3) pi t)
-        at t0 + dt/2 (leapfrog staggering, stepper1d.cpp:131-145), exact jets on
-        the device; dt = cfl h / sqrt(3)."""
+        """Standing mode of the periodic global box, p = cos(wt t) prod_a
+        sin(w_a x_a) with w_a = 2 pi / L_a (on [-1, 1]^3: sin(pi x) sin(pi y)
+        sin(pi z)), and its velocity v_c = -(w_c / wt) sin(wt t) cos(w_c x_c)
+        prod_{a != c} sin(w_a x_a) at t0 + dt/2 (leapfrog staggering,
+        stepper1d.cpp:131-145): an exact solution on any box, exact jets on the
+        device; dt = cfl h / sqrt(3)."""
         s = self.solver
-        pi = math.pi
-        wt = math.sqrt(3.0) * pi
+        w = [2.0 * math.pi / (k * self.h) for k in self.K_global]
+        wt = math.sqrt(sum(x * x for x in w))
         dt = cfl * self.h / math.sqrt(3.0)
         tv = t0 + dt / 2
         for f in range(4):
             s.zero_field(f)
-        s.fill_separable(0, math.cos(wt * t0), [pi] * 3, [0.0] * 3)
+        s.fill_separable(0, math.cos(wt * t0), w, [0.0] * 3)
         for c in range(3):
-            ph = [pi / 2 if a == c else 0.0 for a in range(3)]
-            s.fill_separable(1 + c, -(pi / wt) * math.sin(wt * tv), [pi] * 3, ph)
+            ph = [math.pi / 2 if a == c else 0.0 for a in range(3)]
+            s.fill_separable(1 + c, -(w[c] / wt) * math.sin(wt * tv), w, ph)
         s.set_times(t0, tv, dt)
         return dt
 
