@@ -120,3 +120,16 @@ def test_create_without_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(H.CudaError):
         H.Stepper(H.Grid1d.over(-1.0, 1.0, 8), 2)
+
+
+def test_missing_extension_fails_loudly(tmp_path):
+    # no CPU fallback: without the CUDA library the product path raises
+    import subprocess
+    import sys
+    code = ("import paper_1808_10481_b200 as H\n"
+            "H.Stepper(H.Grid1d.over(-1.0, 1.0, 8), 2)\n")
+    env = dict(os.environ, HLF_B200_LIB_OVERRIDE=str(tmp_path / "absent.so"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
+    assert r.returncode != 0
+    assert "absent.so" in r.stderr and "missing" in r.stderr
