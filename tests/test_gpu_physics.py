@@ -11,6 +11,7 @@ rates and discrete energy conservation") on the tiled sm_100a kernels.
   kernel, and the 3D mode (cfg 4) on the tiled 3D kernel (order band for
   m = 2, error levels for m = 3)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -309,3 +310,75 @@ def test_device_energy_matches_reference(golden, have_ref, m):
         g.advance_v()
         r.set(g.get_field(0), g.get_field(1), g.times())
         assert g.energy_1d(1, 1.0) == pytest.approx(r.conserved_r(1.0), rel=1e-11)
+
+
+def gaussian_pulse_jets(K, h, n1):
+    # gaussian_pulse_problem (problems.cpp:185-199): p = gaussian(0.3, 0.3,
+    # delta = 0.002), velocities at rest; primary grid with walls: (K+1)^2 nodes
+    N = K + 1
+    out = np.zeros((N * N, n1 * n1))
+    for ix in range(N):
+        for iy in range(N):
+            out[ix * N + iy] = O.ref2d_exact("gaussian-pulse", 0, -1.0 + ix * h, -1.0 + iy * h, 0.0, h, n1).ravel()
+    return out
+
+
+def c2_value(x, y):
+    return 1.0 + 0.5 * np.sin(np.pi * x) * np.sin(np.pi * y)
+
+
+@pytest.mark.parametrize("m", [2, 3])
+def test_config3_gaussian_pulse(have_ref, m):
+    # SURVEY sec. 8(d) config 3 at small K: walls, c^2 = 1 + sin(pi x) sin(pi y) / 2
+    # jets (var2d kernel), the reference's Gaussian pulse; parity with the
+    # oracle over 20 steps, then a long run whose c^2-weighted nodal energy
+    # sum(p^2 / c^2 + |v|^2) h^2 stays bounded (no instability, no growth)
+    if not have_ref:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_gpu_parity import c2_jets, make_pair, compare, run_both
+
+    K, bnd = 32, [1, 1]
+    h = 2.0 / K
+    g, o = make_pair(2, m, [K, K], boundary=bnd, variable=True, seed=1)
+    assert g.kernel_variant == 1
+    n = 2 * m + 2
+    for grid, dual in ((0, False), (1, True)):
+        jets = c2_jets(2, [K, K], h, n, bnd, dual)
+        g.set_coeff(grid, jets)
+        o.set_coeff(grid, 0, jets)
+    p0 = gaussian_pulse_jets(K, h, m + 1)
+    for s in (g, o):
+        s.set_field(0, p0)
+        for c in (1, 2):
+            (s.zero_field(c) if s is g else s.set_field(c, np.zeros((K * K, (m + 1) ** 2))))
+    dt = 0.9 * h / (math.sqrt(2) * math.sqrt(1.5))
+    run_both(g, o, 20, dt)
+    compare(g, o, 2)
+
+    # energy run at a resolution that resolves the pulse (width sqrt(delta) ~ 0.045)
+    K = 128
+    h = 2.0 / K
+    g = H.Stepper(H.Grid([-1.0, -1.0], h, (K, K)), m, boundary=bnd, variable_ap=True)
+    for grid, dual in ((0, False), (1, True)):
+        g.set_coeff(grid, c2_jets(2, [K, K], h, n, bnd, dual))
+    g.set_field(0, gaussian_pulse_jets(K, h, m + 1))
+    g.zero_field(1)
+    g.zero_field(2)
+    dt = 0.9 * h / (math.sqrt(2) * math.sqrt(1.5))
+    g.set_times(0.0, dt / 2, dt)
+    x = -1.0 + h * np.arange(K + 1)
+    c2p = c2_value(x[:, None], x[None, :]).ravel()
+
+    def energy():
+        p = g.get_field(0)[:, 0]
+        v = g.get_field(1)[:, 0] ** 2 + g.get_field(2)[:, 0] ** 2
+        return float((p * p / c2p).sum() + v.sum()) * h * h
+
+    g.advance_n(20)
+    e0 = energy()
+    for _ in range(10):
+        g.advance_n(40)
+        e = energy()
+        assert 0.8 * e0 < e < 1.2 * e0, (e, e0)
