@@ -4,7 +4,8 @@ The headline 3D line is bench.py's; this script records the others:
 
   cfg1   1D m=3 standing wave, K=256 (143 steps) and K=2^24
   cfg2   2D periodic acoustics mode, K=1024, m=1..4 (+ 4096^2 m=3)
-  cfg3   2D walls, K=4096, m=3, variable c^2 jets (generic iterated kernel)
+  cfg3   2D walls, K=4096, m=3, c^2 = 1 + sin(pi x) sin(pi y)/2 jets (var2d kernel;
+         separable data instead of the Gaussian pulse: same arithmetic)
   cfg4   3D periodic, 512x512x256, m=1..3 (bench.py's workload)
 
 Usage: python tools/bench_configs.py [out.json]"""
@@ -38,6 +39,24 @@ def timed(g, stream, steps, warm=3):
     return e0.elapsed_time(e1) / steps
 
 
+def sin_jets(x, h, n, w=math.pi):
+    """scaled jets of sin(w x) at the points x: [len(x), n] (sin_jet, jet.cpp)"""
+    k = np.arange(n)
+    fac = np.cumprod(np.concatenate(([1.0], (w * h) / np.arange(1, n))))
+    return fac[None, :] * np.sin(w * x[:, None] + k[None, :] * math.pi / 2)
+
+
+def c2_jets_2d(K, h, n, boundary, dual):
+    """-(1 + sin(pi x) sin(pi y) / 2) jets, [nodes][n * n] x-major (nodes x-slowest)"""
+    N = [K if dual or b == 0 else K + 1 for b in boundary]
+    off = 0.5 * h if dual else 0.0
+    sx = sin_jets(-1.0 + off + h * np.arange(N[0]), h, n)
+    sy = sin_jets(-1.0 + off + h * np.arange(N[1]), h, n)
+    jets = -0.5 * np.einsum("xi,yj->xyij", sx, sy)
+    jets[:, :, 0, 0] -= 1.0
+    return jets.reshape(N[0] * N[1], n * n)
+
+
 def kernel_name(d, variable, variant):
     if d == 1:
         return "faithful1d"  # half_1d: register-resident, bit-identical to the reference
@@ -54,11 +73,12 @@ def run(name, d, m, K, boundary=None, variable=False, steps=20):
     pi = math.pi
     g.fill_separable(0, 1.0, [pi] * d, [0.0] * d)
     if variable:
+        # config 3's ap = -c^2, c^2 = 1 + sin(pi x) sin(pi y) / 2, as scaled jets
+        # (n entries per axis) at the nodes of both grids
         for grid in (0, 1):
-            jets = np.zeros((g.num_nodes(grid), g.E))
-            jets[:, 0] = -1.0  # ap = -c^2 with c^2 = 1 (the iterated variable-coefficient path)
-            g.set_coeff(grid, jets)
-    dt = 0.9 * g.grid.h / math.sqrt(d)
+            g.set_coeff(grid, c2_jets_2d(Ks[0], g.grid.h, 2 * m + 2, boundary or [0, 0], dual=grid == 1))
+    c_max = math.sqrt(1.5) if variable else 1.0
+    dt = 0.9 * g.grid.h / (math.sqrt(d) * c_max)
     g.set_times(0.0, dt / 2, dt)
     ms = timed(g, stream, steps)
     dof = (d + 1) * (m + 1) ** d * math.prod(Ks)
