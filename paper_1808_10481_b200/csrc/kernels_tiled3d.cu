@@ -21,9 +21,11 @@
 // entry any of its 24 (velocity) or 8 (pressure) outputs needs, so the CK sum
 // runs entirely in registers with compile-time indices.
 //
-// VEL (p -> v_x, v_y, v_z) is one launch; PRE (v -> p) is three launches, one
-// per source component c, each adding the c-th divergence term (q_c+1)V_c[q+e_c]
-// through the same code with target component c.
+// VEL (p -> v_x, v_y, v_z) is one launch; PRE (v -> p) is two: the V_x and
+// V_y divergence terms merged (their index shifts moved into the x / y sweep
+// rows, summed in the XY stage, one shift-free CK), and V_z (HLF_NO_MERGE:
+// three launches, one per source component c, each adding the c-th
+// divergence term (q_c+1) V_c[q+e_c] with target component c).
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -53,7 +55,7 @@ struct Cfg {
   static constexpr int RAWS = (RAW + 2 + 15) / 16 * 16;
   static constexpr int RING = n * n * n1 * TXC;
   // NT: 3 = velocity half (three targets), 1 = one pressure divergence term,
-  // 2 = merged V_x + V_y pressure launch (two raw sources, one target; m = 3)
+  // 2 = merged V_x + V_y pressure launch (two raw sources, one target)
   template <int NT>
   static constexpr int NTGT = NT == 2 ? 1 : NT;
   template <int NT>
