@@ -22,7 +22,8 @@ def _coeffs(r):
 
 @pytest.mark.parametrize("problem", ["standing-wave", "random-wave"])
 @pytest.mark.parametrize("m", [0, 1, 2, 3, 5])
-def test_modified_scheme_matches_reference(have_ref, problem, m):
+@pytest.mark.parametrize("chunk", [0, 8])  # 8: advance_n replays CUDA graphs of 8 steps
+def test_modified_scheme_matches_reference(have_ref, problem, m, chunk):
     if not have_ref:
         pytest.skip("compiled reference (oracle/_ref) not built")
     K = 40
@@ -32,6 +33,7 @@ def test_modified_scheme_matches_reference(have_ref, problem, m):
     (pp, vp, pd, vd), (t, dt) = r.get_modified()
     ap, av = _coeffs(r)
     g = H.Stepper(H.Grid1d.over(-1.0, 1.0, K), m, ap=ap, av=av, scheme=H.SCHEME_MODIFIED)
+    g.set_graph_steps(chunk)
     for f, a in ((0, pp), (1, vd), (2, vp), (3, pd)):
         g.set_field(f, a)
     g.set_times(t, t + dt / 2, dt)
@@ -46,7 +48,8 @@ def test_modified_scheme_matches_reference(have_ref, problem, m):
 
 @pytest.mark.parametrize("problem", ["standing-wave", "random-wave"])
 @pytest.mark.parametrize("m", [0, 1, 2, 3, 5])
-def test_dual_hermite_scheme_matches_reference(have_ref, problem, m):
+@pytest.mark.parametrize("chunk", [0, 8])  # 8: advance_n replays CUDA graphs of 8 steps
+def test_dual_hermite_scheme_matches_reference(have_ref, problem, m, chunk):
     if not have_ref:
         pytest.skip("compiled reference (oracle/_ref) not built")
     K = 40
@@ -56,6 +59,7 @@ def test_dual_hermite_scheme_matches_reference(have_ref, problem, m):
     (p, v), (t, dt) = r.get_dual()
     ap, av = _coeffs(r)
     g = H.Stepper(H.Grid1d.over(-1.0, 1.0, K), m, ap=ap, av=av, scheme=H.SCHEME_DUAL_HERMITE)
+    g.set_graph_steps(chunk)
     g.set_field(0, p)
     g.set_field(2, v)
     g.set_times(t, t, dt)
