@@ -66,6 +66,19 @@ class DeviceStepper {
     check(hlf_set_forcing(s_, grid, table.data()), s_);
   }
   void clear_forcing() { check(hlf_clear_forcing(s_), s_); }
+  // advance_n replays chunks of `steps` steps as one CUDA graph (0: off)
+  void set_graph_steps(int steps) { check(hlf_set_graph_steps(s_, steps), s_); }
+  // on-device accessors (analysis.cpp:221-285)
+  double l2_error_separable(int field, double amp, const double* w, const double* phase) {
+    double l2 = 0.0;
+    check(hlf_l2_error_separable(s_, field, amp, w, phase, &l2), s_);
+    return l2;
+  }
+  double energy_1d(int kind, double c) {
+    double e = 0.0;
+    check(hlf_energy_1d(s_, kind, c, &e), s_);
+    return e;
+  }
   void set_times(double t_p, double t_v, double dt) { check(hlf_set_times(s_, t_p, t_v, dt), s_); }
   void times(double& t_p, double& t_v, double& dt) const { check(hlf_get_times(s_, &t_p, &t_v, &dt), s_); }
   void set_dt(double dt) { check(hlf_set_dt(s_, dt), s_); }
