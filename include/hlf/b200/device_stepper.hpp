@@ -87,6 +87,12 @@ class DeviceStepper {
   void advance_v() { check(hlf_advance_v(s_), s_); }
   void step(int step_index) { check(hlf_step(s_, step_index), s_); }
   void advance_n(int n, int first_step) { check(hlf_advance_n(s_, n, first_step), s_); }
+  // from t_p to T in steps of the current dt (hlf_advance_to); returns the steps run
+  int advance_to(double T, int first_step) {
+    int n = 0;
+    check(hlf_advance_to(s_, T, first_step, &n), s_);
+    return n;
+  }
   void synchronize() { check(hlf_synchronize(s_), s_); }
 
   hlf_solver* handle() const { return s_; }

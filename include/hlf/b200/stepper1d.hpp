@@ -27,6 +27,7 @@
 // (the reference's CPU Stepper1d still covers it).
 #pragma once
 
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -129,6 +130,27 @@ class Stepper1d {
     upload(st);
     guarded([&] { forced_or_plain_steps(st, n, first_step); }, st);
     download(st);
+  }
+  // extension: from st.t_p to T in steps of st.dt, i.e. the caller loop of
+  // test_stepper1d.cpp:33-38 (dt = T / step_count(T, dt_nominal) chosen before
+  // init_leapfrog); returns the steps run.  ConfigError when st.dt does not
+  // divide T - t_p (the staggered v sits half a step of that dt away).
+  int advance_to(State1d& st, double T, int first_step = 0) const {
+    if (prob_.forcing) {
+      // forcing tables are evaluated per half step on the host: the same
+      // step rule as hlf_advance_to, then the forced steps one by one
+      const double q = st.dt != 0.0 ? (T - st.t_p) / st.dt : -1.0;
+      const double nr = std::nearbyint(q);
+      if (!(q > -1e-9) || std::fabs(q - nr) > 1e-9 * std::fmax(1.0, std::fabs(q)))
+        throw ConfigError("dt does not divide T - t_p; initialise the state with dt = T / step_count(T, dt_nominal)");
+      advance_n(st, static_cast<int>(nr), first_step);
+      return static_cast<int>(nr);
+    }
+    upload(st);
+    int n = 0;
+    guarded([&] { n = dev_->advance_to(T, first_step); }, st);
+    download(st);
+    return n;
   }
 
   // ---- modified Hermite-leapfrog (stepper1d.cpp:174-232)

@@ -20,6 +20,8 @@
  *   hlf_advance_v              <- Stepper1d::advance_v          stepper1d.hpp:73, stepper1d.cpp:158-166
  *   hlf_step                   <- Stepper1d::step_system        stepper1d.hpp:74, stepper1d.cpp:168-172
  *   hlf_advance_n              <- the caller's step loop        tests/test_stepper1d.cpp:38
+ *   hlf_plan_steps             <- step_count + dt = T / n       config.cpp:34-38, tests/test_stepper1d.cpp:33-35
+ *   hlf_advance_to             <- the caller loop up to T       tests/test_stepper1d.cpp:33-38
  *   hlf_poll_finite            <- Stepper1d::check_finite       stepper1d.cpp:121-129
  *   status codes               <- ConfigError, InstabilityError config.hpp:15-24, std::invalid_argument
  *
@@ -149,6 +151,19 @@ hlf_status hlf_step(hlf_solver* s, int step_index);
 /* n steps indexed first..first+n-1; the finite flag is read once at the end and
    the first offending step index is reported through HLF_INSTABILITY */
 hlf_status hlf_advance_n(hlf_solver* s, int n, int first_step);
+/* The caller's step rule (step_count, config.hpp:47 / config.cpp:34-38, and
+   tests/test_stepper1d.cpp:33-35): n = ceil(T / dt_nominal), dt = T / n.
+   HLF_CONFIG_ERROR for T <= 0 or dt_nominal <= 0, as step_count throws. */
+hlf_status hlf_plan_steps(double T, double dt_nominal, int* n_out, double* dt_out);
+/* Advance from the current t_p to T in steps of the current dt (the reference
+   has no advance-to; this is its caller loop `for i < nsteps: step_system(st,
+   i)`, test_stepper1d.cpp:38): n = (T - t_p) / dt steps indexed first_step..,
+   through hlf_advance_n.  dt is fixed by the staggered initialisation
+   (init_leapfrog sets t_v = t0 + dt/2, stepper1d.cpp:137), so it must divide
+   T - t_p to 1e-9 relative (HLF_CONFIG_ERROR otherwise; use hlf_plan_steps to
+   pick dt before initialising).  Negative dt runs backwards to T < t_p.
+   *steps_out = the steps run. */
+hlf_status hlf_advance_to(hlf_solver* s, double T, int first_step, int* steps_out);
 /* -1 when the state stayed finite, else the first non-finite step index */
 /* hlf_advance_n replays runs of `steps` leapfrog steps as one captured CUDA
    graph (launch overhead dominates small grids); 0 = launch every kernel
@@ -201,6 +216,20 @@ hlf_status hlf_halo_recv_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr
 
 /* number of kernels this solver has launched (for launch accounting) */
 int64_t hlf_launch_count(const hlf_solver* s);
+/* Path accounting of the tiled 2D/3D kernels (tests): when enabled (and reset
+   by enabling again) every CTA of a tiled launch counts itself, per half step
+   kind (0 = velocity, 1 = pressure): out6 = [vel CTAs, vel CTAs whose source
+   rows arrived by TMA boxes, vel CTAs whose targets arrived by TMA boxes, the
+   same three for the pressure launches].  Off by default (no cost). */
+hlf_status hlf_enable_path_counters(hlf_solver* s, int on);
+/* Per-launch device times: runs `steps` leapfrog steps (indexed first_step..,
+   advancing the state and the time stamps like hlf_step without the finite
+   check) with CUDA events on the solver's stream around every kernel of each
+   half step, synchronising after each half step.  ms_out[0..2] = mean ms of
+   the velocity half step's launches 0..2, ms_out[3..5] = the pressure half
+   step's; launches_out[0..1] = launches per velocity / pressure half step. */
+hlf_status hlf_time_launches(hlf_solver* s, int steps, int first_step, double* ms_out, int* launches_out);
+hlf_status hlf_read_path_counters(hlf_solver* s, int64_t* out6);
 /* kernel variant the next half steps use: 0 generic, 1 tiled 3D */
 int hlf_kernel_variant(const hlf_solver* s);
 hlf_status hlf_set_kernel_variant(hlf_solver* s, int variant);

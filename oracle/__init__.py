@@ -22,6 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libhlf_refc.so")
 ORACLE_SO = os.path.join(HERE, "_build", "libhlf_oracle.so")
+ORACLE_FMA_SO = os.path.join(HERE, "_build", "libhlf_oracle_fma.so")
 REF_TESTS = [os.path.join(HERE, "_ref", t) for t in ("test_jet", "test_interpolation", "test_stepper1d")]
 
 _dp = C.POINTER(C.c_double)
@@ -43,6 +44,7 @@ def _ptr(a: np.ndarray):
 
 _ref_lib = None
 _orc_lib = None
+_orc_fma_lib = None
 
 
 def ref_available() -> bool:
@@ -103,12 +105,16 @@ def ref_lib():
     return _ref_lib
 
 
-def orc_lib():
-    global _orc_lib
-    if _orc_lib is None:
-        if not os.path.exists(ORACLE_SO):
-            raise FileNotFoundError(f"{ORACLE_SO} missing: run `make -C oracle oracle`")
-        L = C.CDLL(ORACLE_SO)
+def orc_lib(fma: bool = False):
+    """The restatement; fma=True loads the build with compiler-contracted FMAs
+    (same algorithm, another valid rounding: the long-run drift yardstick)."""
+    global _orc_lib, _orc_fma_lib
+    cached = _orc_fma_lib if fma else _orc_lib
+    if cached is None:
+        so = ORACLE_FMA_SO if fma else ORACLE_SO
+        if not os.path.exists(so):
+            raise FileNotFoundError(f"{so} missing: run `make -C oracle oracle`")
+        L = C.CDLL(so)
         L.orc_create.argtypes = [C.c_int, C.c_int, _ip, _ip, C.c_double, C.c_double, C.c_double, C.c_int]
         L.orc_create.restype = C.c_void_p
         L.orc_destroy.argtypes = [C.c_void_p]
@@ -130,8 +136,12 @@ def orc_lib():
         L.orc_get_layer.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp]
         L.orc_set_halo.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp]
         L.orc_add_separable.argtypes = [C.c_int, _ip, _dp, C.c_double, C.c_double, C.c_int, C.c_double, _dp, _dp, _dp]
-        _orc_lib = L
-    return _orc_lib
+        if fma:
+            _orc_fma_lib = L
+        else:
+            _orc_lib = L
+        cached = L
+    return cached
 
 
 # ---------------------------------------------------------------- reference
@@ -304,8 +314,8 @@ class OracleStepper:
     Fields: 0 = p on the primary grid, 1..d = velocity components on the dual
     grid.  Host layout [node][coef], both x-major."""
 
-    def __init__(self, d, m, K, h, boundary=None, ap=-1.0, av=-1.0, threads=None):
-        self.L = orc_lib()
+    def __init__(self, d, m, K, h, boundary=None, ap=-1.0, av=-1.0, threads=None, fma=False):
+        self.L = orc_lib(fma)
         self.d, self.m = d, m
         K = list(K) if hasattr(K, "__len__") else [K] * d
         boundary = list(boundary) if boundary is not None else [0] * d

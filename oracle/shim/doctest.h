@@ -14,6 +14,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <exception>
 #include <functional>
 #include <string>
@@ -124,6 +125,12 @@ inline int run_all() {
 #define TEST_CASE(name) DOCTEST_TC_IMPL(DOCTEST_CAT(doctest_tc_, __COUNTER__), name)
 #define SUBCASE(name) if (true)
 #define CAPTURE(x) ((void)0)
+#define MESSAGE(msg)                                                    \
+  do {                                                                  \
+    std::ostringstream doctest_os_;                                     \
+    doctest_os_ << msg;                                                 \
+    std::printf("[doctest-shim] %s\n", doctest_os_.str().c_str());      \
+  } while (0)
 #define CHECK(...) ::doctest::detail::report(static_cast<bool>(__VA_ARGS__), "CHECK", #__VA_ARGS__, __FILE__, __LINE__)
 #define REQUIRE(...)                                                                      \
   do {                                                                                    \

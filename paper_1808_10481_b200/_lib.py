@@ -22,10 +22,11 @@ EXPORTS = [
     "hlf_num_nodes", "hlf_num_coeffs", "hlf_set_field", "hlf_get_field", "hlf_set_coeff",
     "hlf_set_forcing", "hlf_clear_forcing", "hlf_set_graph_steps", "hlf_l2_error_separable", "hlf_energy_1d",
     "hlf_set_times", "hlf_get_times", "hlf_set_dt", "hlf_advance_p", "hlf_advance_v", "hlf_step",
-    "hlf_advance_n", "hlf_advance_p_indexed", "hlf_advance_v_indexed", "hlf_advance_layers", "hlf_commit_half",
+    "hlf_advance_n", "hlf_plan_steps", "hlf_advance_to", "hlf_advance_p_indexed", "hlf_advance_v_indexed", "hlf_advance_layers", "hlf_commit_half",
     "hlf_poll_finite", "hlf_clear_finite", "hlf_synchronize", "hlf_field_device",
     "hlf_fill_separable", "hlf_error_separable", "hlf_zero_field", "hlf_halo_send_ptr", "hlf_halo_recv_ptr",
-    "hlf_launch_count", "hlf_kernel_variant", "hlf_set_kernel_variant",
+    "hlf_launch_count", "hlf_kernel_variant", "hlf_set_kernel_variant", "hlf_enable_path_counters",
+    "hlf_read_path_counters", "hlf_time_launches",
 ]
 
 
@@ -84,6 +85,8 @@ def lib() -> C.CDLL:
         "hlf_advance_v": ([S], st),
         "hlf_step": ([S, C.c_int], st),
         "hlf_advance_n": ([S, C.c_int, C.c_int], st),
+        "hlf_plan_steps": ([C.c_double, C.c_double, C.POINTER(C.c_int), _dp], st),
+        "hlf_advance_to": ([S, C.c_double, C.c_int, C.POINTER(C.c_int)], st),
         "hlf_advance_p_indexed": ([S, C.c_int], st),
         "hlf_advance_v_indexed": ([S, C.c_int], st),
         "hlf_advance_layers": ([S, C.c_int, C.c_int, C.c_int, C.c_int], st),
@@ -103,6 +106,9 @@ def lib() -> C.CDLL:
         "hlf_launch_count": ([S], C.c_int64),
         "hlf_kernel_variant": ([S], C.c_int),
         "hlf_set_kernel_variant": ([S, C.c_int], st),
+        "hlf_enable_path_counters": ([S, C.c_int], st),
+        "hlf_read_path_counters": ([S, C.POINTER(C.c_int64)], st),
+        "hlf_time_launches": ([S, C.c_int, C.c_int, _dp, C.POINTER(C.c_int)], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

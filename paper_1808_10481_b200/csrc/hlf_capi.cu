@@ -55,6 +55,10 @@ struct hlf_solver {
   bool force_fresh[2] = {false, false};
   int* flag = nullptr;
   int* flag_host = nullptr;
+  unsigned long long* path_ctr = nullptr;  // hlf_enable_path_counters (tests)
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};  // hlf_time_launches
+  bool timing = false;
+  int tev_idx = 0;
   double* errbuf = nullptr;     // hlf_error_separable accumulator (device) and its host copy
   double* errbuf_host = nullptr;
   double* staging[2] = {nullptr, nullptr};  // double-buffered host-transfer staging
@@ -334,6 +338,13 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
   P.c_layer = s->plane[tf] * s->E;
   P.step = step;
   P.flag = s->flag;
+  P.path_ctr = s->path_ctr;
+  if (s->timing) {
+    s->tev_idx = 0;
+    P.launch_ev = s->tev;
+    P.launch_idx = &s->tev_idx;
+    HLF_CUDA(s, cudaEventRecord(s->tev[0], s->stream));
+  }
   const int fg = s->grid_of(tf);
   if (s->force_on) {
     if (!s->force_fresh[fg])
@@ -363,6 +374,7 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
   if (launched == -2 || launched < 0 && s->variant != 1)  // -2: custom M / planes too large for the tiled kernel
     launched = hlfk::launch_half_generic(s->d, s->m, s->variable, kind, P, s->stream);
   if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
+  if (s->timing && s->tev_idx == 0) mark_launch(P, s->stream);  // kernels without their own marks
   s->launches += launched;
   HLF_CUDA(s, cudaGetLastError());
   if (s->force_on) s->force_fresh[fg] = false;
@@ -512,6 +524,9 @@ void hlf_destroy(hlf_solver* s) {
     if (c) cudaFree(c);
   if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
   if (s->flag) cudaFree(s->flag);
+  if (s->path_ctr) cudaFree(s->path_ctr);
+  for (cudaEvent_t e : s->tev)
+    if (e) cudaEventDestroy(e);
   if (s->flag_host) cudaFreeHost(s->flag_host);
   if (s->errbuf) cudaFree(s->errbuf);
   if (s->errbuf_host) cudaFreeHost(s->errbuf_host);
@@ -730,6 +745,17 @@ static hlf_status step_async(hlf_solver* s, int step_index) {
 }
 
 __global__ void set_graph_step_base(int* flag, int base) { flag[1] = base; }
+// flag[0] = INT_MAX (no non-finite value seen): every hlf_step / hlf_advance_n
+// checks only the steps it runs, as check_finite (stepper1d.cpp:121-129) looks
+// only at the current state
+__global__ void reset_finite_flag(int* flag) { flag[0] = INT_MAX; }
+
+static hlf_status reset_flag(hlf_solver* s) {
+  reset_finite_flag<<<1, 1, 0, s->stream>>>(s->flag);
+  s->launches += 1;
+  HLF_CUDA(s, cudaGetLastError());
+  return HLF_OK;
+}
 
 // host time stamps of one step, as step_async / scheme1d_step advance them
 static void advance_times(hlf_solver* s) {
@@ -783,7 +809,9 @@ hlf_status hlf_set_graph_steps(hlf_solver* s, int steps) {
 hlf_status hlf_step(hlf_solver* s, int step_index) {
   if (!s) return HLF_INVALID_ARGUMENT;
   cudaSetDevice(s->device);
-  hlf_status st = step_async(s, step_index);
+  hlf_status st = reset_flag(s);
+  if (st != HLF_OK) return st;
+  st = step_async(s, step_index);
   if (st != HLF_OK) return st;
   int bad = -1;
   st = read_flag(s, &bad);
@@ -795,6 +823,10 @@ hlf_status hlf_advance_n(hlf_solver* s, int n, int first_step) {
   if (!s) return HLF_INVALID_ARGUMENT;
   if (n < 0) return fail(s, HLF_INVALID_ARGUMENT, "negative step count");
   cudaSetDevice(s->device);
+  {
+    hlf_status st = reset_flag(s);
+    if (st != HLF_OK) return st;
+  }
   int i = 0;
   const int chunk = s->graph_chunk;
   if (chunk > 0 && n >= 2 * chunk && !s->force_on && !s->z_slab) {
@@ -824,6 +856,39 @@ hlf_status hlf_advance_n(hlf_solver* s, int n, int first_step) {
   hlf_status st = read_flag(s, &bad);
   if (st != HLF_OK) return st;
   return bad >= 0 ? instability(s, bad) : HLF_OK;
+}
+
+hlf_status hlf_plan_steps(double T, double dt_nominal, int* n_out, double* dt_out) {
+  // step_count (config.cpp:34-38) and the caller's dt = T / n (tests/test_stepper1d.cpp:33-35)
+  if (!(T > 0.0)) return fail(nullptr, HLF_CONFIG_ERROR, "final time must be positive");
+  if (!(dt_nominal > 0.0)) return fail(nullptr, HLF_CONFIG_ERROR, "nominal dt must be positive");
+  const double q = std::ceil(T / dt_nominal);
+  if (!(q < 2147483647.0)) return fail(nullptr, HLF_CONFIG_ERROR, "step count overflows int");
+  const int n = static_cast<int>(q);
+  if (n_out) *n_out = n;
+  if (dt_out) *dt_out = T / n;
+  return HLF_OK;
+}
+
+hlf_status hlf_advance_to(hlf_solver* s, double T, int first_step, int* steps_out) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  if (steps_out) *steps_out = 0;
+  const double span = T - s->t_p;
+  if (!(s->dt != 0.0) || !std::isfinite(s->dt) || !std::isfinite(T))
+    return fail(s, HLF_CONFIG_ERROR, "advance_to needs a finite nonzero dt and T");
+  const double q = span / s->dt;
+  if (q < -1e-9) return fail(s, HLF_CONFIG_ERROR, "T lies behind the state's time in the direction of dt");
+  const double nr = std::nearbyint(q);
+  // the staggered partner was initialised half a step of this dt away
+  // (init_leapfrog, stepper1d.cpp:131-145): dt cannot change here, so it has
+  // to divide the remaining time
+  if (std::fabs(q - nr) > 1e-9 * std::max(1.0, std::fabs(q)) || nr > 2147483647.0)
+    return fail(s, HLF_CONFIG_ERROR,
+                "dt does not divide T - t_p; initialise the state with dt = T / step_count(T, dt_nominal)");
+  const int n = static_cast<int>(nr);
+  hlf_status st = hlf_advance_n(s, n, first_step);
+  if (steps_out) *steps_out = n;
+  return st;
 }
 
 hlf_status hlf_poll_finite(hlf_solver* s, int* first_bad_step) {
@@ -1069,6 +1134,75 @@ hlf_status hlf_halo_recv_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr
 }
 
 int64_t hlf_launch_count(const hlf_solver* s) { return s ? s->launches : -1; }
+
+hlf_status hlf_enable_path_counters(hlf_solver* s, int on) {
+  if (!s) return HLF_INVALID_ARGUMENT;
+  cudaSetDevice(s->device);
+  if (on) {
+    if (!s->path_ctr) HLF_CUDA(s, cudaMalloc(&s->path_ctr, 6 * sizeof(unsigned long long)));
+    HLF_CUDA(s, cudaMemsetAsync(s->path_ctr, 0, 6 * sizeof(unsigned long long), s->stream));
+  } else if (s->path_ctr) {
+    HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+    cudaFree(s->path_ctr);
+    s->path_ctr = nullptr;
+  }
+  s->gen++;  // a captured graph holds the old parameter blocks
+  return HLF_OK;
+}
+
+hlf_status hlf_time_launches(hlf_solver* s, int steps, int first_step, double* ms_out, int* launches_out) {
+  if (!s || !ms_out || steps <= 0) return HLF_INVALID_ARGUMENT;
+  if (s->scheme != HLF_SCHEME_LEAPFROG) return fail(s, HLF_CONFIG_ERROR, "launch timing covers the leapfrog scheme");
+  cudaSetDevice(s->device);
+  for (cudaEvent_t& e : s->tev)
+    if (!e) HLF_CUDA(s, cudaEventCreate(&e));
+  double acc[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  int nl[2] = {0, 0};
+  s->timing = true;
+  hlf_status st = HLF_OK;
+  for (int i = 0; i < steps && st == HLF_OK; ++i) {
+    // step_system order: pressure (advance_p) then velocity (advance_v)
+    for (int half = 0; half < 2 && st == HLF_OK; ++half) {
+      const hlfk::HalfKind kind = half == 0 ? hlfk::PRE : hlfk::VEL;
+      st = launch_half(s, kind, first_step + i);
+      if (st != HLF_OK) break;
+      if (half == 0) s->t_p += s->dt;
+      else s->t_v += s->dt;
+      const int k = kind == hlfk::VEL ? 0 : 1;
+      nl[k] = s->tev_idx;
+      if (cudaEventSynchronize(s->tev[s->tev_idx]) != cudaSuccess) {
+        st = cuda_fail(s, cudaGetLastError(), "launch timing");
+        break;
+      }
+      for (int j = 0; j < s->tev_idx; ++j) {
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, s->tev[j], s->tev[j + 1]);
+        acc[k][j] += ms;
+      }
+    }
+  }
+  s->timing = false;
+  if (st != HLF_OK) return st;
+  for (int k = 0; k < 2; ++k)
+    for (int j = 0; j < 3; ++j) ms_out[3 * k + j] = j < nl[k] ? acc[k][j] / steps : 0.0;
+  if (launches_out) {
+    launches_out[0] = nl[0];
+    launches_out[1] = nl[1];
+  }
+  return HLF_OK;
+}
+
+hlf_status hlf_read_path_counters(hlf_solver* s, int64_t* out6) {
+  if (!s || !out6) return HLF_INVALID_ARGUMENT;
+  cudaSetDevice(s->device);
+  unsigned long long h[6] = {0, 0, 0, 0, 0, 0};
+  if (s->path_ctr) {
+    HLF_CUDA(s, cudaMemcpyAsync(h, s->path_ctr, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
+    HLF_CUDA(s, cudaStreamSynchronize(s->stream));
+  }
+  for (int i = 0; i < 6; ++i) out6[i] = static_cast<int64_t>(h[i]);
+  return HLF_OK;
+}
 int hlf_kernel_variant(const hlf_solver* s) { return s ? s->variant : -1; }
 
 hlf_status hlf_set_kernel_variant(hlf_solver* s, int variant) {

@@ -49,7 +49,27 @@ struct HalfParams {
   int bnd[3];                   // 0 periodic, 1 reflective (x, y in-kernel; z via ghost layers)
   int step;                     // step index for the finite flag, -1 = do not record
   int* flag;                    // [first non-finite step (atomicMin), graph step base]
+  // optional path counters (tests; null in production): per HalfKind
+  // [CTAs, CTAs that loaded their source rows by TMA, CTAs that loaded their targets by TMA]
+  unsigned long long* path_ctr;
+  // optional per-launch timing (hlf_time_launches): event launch_ev[i + 1] is
+  // recorded after the i-th kernel of this half step (launch_ev[0] before it)
+  cudaEvent_t* launch_ev;
+  int* launch_idx;
 };
+
+// record the "after launch" event of a timed half step (no-op otherwise)
+inline void mark_launch(const HalfParams& p, cudaStream_t st) {
+  if (p.launch_ev != nullptr && *p.launch_idx < 3) cudaEventRecord(p.launch_ev[++*p.launch_idx], st);
+}
+
+// per-CTA path accounting of the tiled kernels (counters enabled by hlf_enable_path_counters)
+__device__ __forceinline__ void count_path(unsigned long long* ctr, bool tma_rows, bool tma_t) {
+  if (ctr == nullptr) return;
+  atomicAdd(ctr, 1ull);
+  if (tma_rows) atomicAdd(ctr + 1, 1ull);
+  if (tma_t) atomicAdd(ctr + 2, 1ull);
+}
 
 struct FillParams {
   double* dst;

@@ -51,6 +51,8 @@ struct T2Params {
   int zc;                       // target rows per CTA
   int tma, tma_t;                  // tensor maps encoded (raw sources / targets)
   int* flag;
+  unsigned long long* ctr;         // path counters of this half step (tests) or null
+  const HalfParams* hp;            // host only: the caller's parameters (launch timing)
 };
 
 #include "tiled2d_gen.cuh"
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(NTHREADS) tiled2d(const __grid_constant__ T2Pa
       mbar_init(&tgtbar[i], 1);
     }
     fence_mbar_init();
+    count_path(P.ctr, tma_rows, P.tma_t != 0);
   }
   __syncthreads();
 
@@ -386,6 +389,7 @@ int launch_one(T2Params T, cudaStream_t st) {
   T.zc = zc_env > 0 ? zc_env : (ctas32 >= 2048 ? ZC : (MM == 1 ? 8 : (MM == 2 ? ZC : 16)));
   dim3 grid((T.tNx + TXC - 1) / TXC, (T.tNy + T.zc - 1) / T.zc);
   tiled2d<MM, NT><<<grid, NTHREADS, smem, st>>>(T);
+  mark_launch(*T.hp, st);
   return 1;
 }
 
@@ -414,6 +418,8 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.bnd[1] = p.bnd[1];
   T.step = p.step;
   T.flag = p.flag;
+  T.ctr = p.path_ctr ? p.path_ctr + 3 * kind : nullptr;
+  T.hp = &p;
   if (kind == VEL) {
     T.src = p.src[0];
     T.dst[0] = p.dst[0];

@@ -95,6 +95,8 @@ struct TParams {
   int tma;                         // strides allow 16 B aligned TMA row copies
   int tma_t;                       // target tensor maps encoded
   int* flag;
+  unsigned long long* ctr;         // path counters of this half step (tests) or null
+  const HalfParams* hp;            // host only: the caller's parameters (launch timing)
 };
 
 __host__ __device__ constexpr int bindex(int b0, int b1, int b2, int mm) {
@@ -327,6 +329,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     mbar_init(&rawbar[1], 1);
     mbar_init(&tgtbar, 1);
     fence_mbar_init();
+    count_path(P.ctr, tma_rows, P.tma_t != 0);
   }
   __syncthreads();
   constexpr int ROWS = 2 * F;
@@ -666,6 +669,7 @@ int launch_one(TParams T, cudaStream_t st) {
   ensure_smem_opt_in(tiled3d<MM, NT>, static_cast<int>(smem), configured);
   dim3 grid((T.tNx + TXC - 1) / TXC, T.tNy, (T.tNz + ZC - 1) / ZC);
   tiled3d<MM, NT><<<grid, NTHREADS, smem, st>>>(T);
+  mark_launch(*T.hp, st);
   return 1;
 }
 
@@ -701,6 +705,8 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.bnd[1] = p.bnd[1];
   T.step = p.step;
   T.flag = p.flag;
+  T.ctr = p.path_ctr ? p.path_ctr + 3 * kind : nullptr;
+  T.hp = &p;
   // TMA boxes: 16 B aligned strides and bases (checked again per tensor map)
   T.tma = std::getenv("HLF_NO_TMA") == nullptr && p.s_layer % 2 == 0 && p.s_coef % 2 == 0 && p.sNx % 2 == 0;
   T.tma_t = std::getenv("HLF_NO_TMA_T") == nullptr;

@@ -138,7 +138,14 @@ class SlabStepper:
         self.stream = stream
         x0 = (x_min[0], x_min[1], x_min[2] + rank * self.kz * h)
         grid = Grid(x0, h, (Kx, Ky, self.kz))
-        sptr = stream.cuda_stream if stream is not None else None
+        if stream is None:
+            # the solver and the NCCL halos must share one stream (halo sends
+            # follow the kernels that write the sent layer; kernels follow the
+            # receives): give the solver a torch stream the exchange runs under
+            import torch
+            stream = torch.cuda.Stream(device=device)
+        self.stream = stream
+        sptr = stream.cuda_stream
         self.solver = Stepper(grid, m, device=device, stream=sptr, z_slab=world > 1)
         self.halo = None
         if world > 1:
@@ -172,11 +179,8 @@ class SlabStepper:
     # ---- stepping
     def step(self, step_index: int):
         import torch
-        if self.stream is not None:
-            # NCCL orders the halo transfers after the solver stream's queued work
-            with torch.cuda.stream(self.stream):
-                slab_step(self.solver, self.halo, step_index)
-        else:
+        # NCCL orders the halo transfers after the solver stream's queued work
+        with torch.cuda.stream(self.stream):
             slab_step(self.solver, self.halo, step_index)
 
     def launch_count(self) -> int:
@@ -186,34 +190,12 @@ class SlabStepper:
         return self.solver.poll_finite()
 
     def kernel_times(self, steps: int = 2):
-        """Device time of the pressure half step (2 launches at m = 3: V_x+V_y
-        merged, V_z) and the velocity half step (1 launch), CUDA events on the
-        solver stream."""
-        import torch
-        st = self.stream or torch.cuda.current_stream()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        pre = vel = 0.0
-        with torch.cuda.stream(st):  # NCCL halos ordered after the solver stream's work
-            for i in range(steps):
-                pre_i, vel_i = self._timed_step(ev, st)
-                pre += pre_i
-                vel += vel_i
-        return {"pre_ms": pre / steps, "vel_ms": vel / steps}
-
-    def _timed_step(self, ev, st):
-        """one step with the halos outside the timed kernels; (pressure ms, velocity ms)"""
-        if self.halo:
-            self.halo.exchange_v()
-        ev[0].record(st)
-        self.solver.advance_p_indexed(-1)
-        ev[1].record(st)
-        if self.halo:
-            self.halo.exchange_p()
-            ev[1].record(st)
-        self.solver.advance_v_indexed(-1)
-        ev[2].record(st)
-        ev[2].synchronize()
-        return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+        """Mean device ms of every launch of the velocity half step (1 launch at
+        m = 3) and the pressure half step (2: V_x+V_y merged, V_z), from CUDA
+        events the library records around each kernel on the solver stream
+        (hlf_time_launches; one rank's kernels, halos not included)."""
+        t = self.solver.time_launches(steps, 10_000)
+        return {"vel": t["vel"], "pre": t["pre"], "vel_ms": sum(t["vel"]), "pre_ms": sum(t["pre"])}
 
     def e2e(self, steps: int, dof_per_step: int):
         """End to end through the C-ABI: upload the staggered state from pinned

@@ -73,6 +73,16 @@ def step_count(T: float, dt_nominal: float) -> int:
     return int(math.ceil(T / dt_nominal))
 
 
+def plan_steps(T: float, dt_nominal: float):
+    """(n, dt) of the reference's caller rule: n = step_count(T, dt_nominal),
+    dt = T / n (config.cpp:34-38, tests/test_stepper1d.cpp:33-35), computed by
+    the C-ABI (hlf_plan_steps)."""
+    n = C.c_int(0)
+    dt = C.c_double(0.0)
+    _check(_L.lib().hlf_plan_steps(T, dt_nominal, C.byref(n), C.byref(dt)), None)
+    return n.value, dt.value
+
+
 # time schemes (hlf::Variant, config.hpp:9; hlf_b200.h HLF_SCHEME_*)
 SCHEME_LEAPFROG, SCHEME_MODIFIED, SCHEME_DUAL_HERMITE = 0, 1, 2
 
@@ -349,13 +359,16 @@ class Stepper:
     def advance_n(self, n: int, first_step: int = 0):
         self._c(self._L.hlf_advance_n(self._h, n, first_step))
 
-    def advance_to(self, T: float, cfl: float = 0.9, c_max: float = 1.0, t0: float | None = None) -> int:
-        """Run to T with n = step_count(T, dt_nominal) steps of dt = T/n,
-        the caller loop of tests/test_stepper1d.cpp:29-38."""
-        cfg = SchemeConfig(m=self.m, cfl=cfl)
-        n = step_count(T, cfg.dt_nominal(self.dim, self.grid.h, c_max))
-        self.advance_n(n, 0)
-        return n
+    def advance_to(self, T: float, first_step: int = 0) -> int:
+        """Advance from the current t_p to T in steps of the current dt, indexed
+        first_step.. (hlf_advance_to): the caller loop of
+        tests/test_stepper1d.cpp:33-38.  dt is fixed when the staggered state is
+        initialised (init_leapfrog, stepper1d.cpp:131-145), so it must divide
+        T - t_p; pick it with plan_steps(T, dt_nominal) first.  Returns the
+        number of steps run; ConfigError if dt does not divide T - t_p."""
+        n = C.c_int(0)
+        self._c(self._L.hlf_advance_to(self._h, T, first_step, C.byref(n)))
+        return n.value
 
     def poll_finite(self) -> int:
         bad = C.c_int(-1)
@@ -416,6 +429,28 @@ class Stepper:
         fn = self._L.hlf_halo_send_ptr if send else self._L.hlf_halo_recv_ptr
         self._c(fn(self._h, kind, comp, C.byref(ptr), C.byref(cnt)))
         return ptr.value, cnt.value
+
+    def enable_path_counters(self, on: bool = True):
+        """Count the CTAs of the tiled kernels and which of them took the TMA
+        box loads (hlf_enable_path_counters; enabling again resets)."""
+        self._c(self._L.hlf_enable_path_counters(self._h, int(on)))
+
+    def time_launches(self, steps: int = 2, first_step: int = 0) -> dict:
+        """Mean device ms of every kernel launch of the two half steps over
+        `steps` leapfrog steps (hlf_time_launches; CUDA events on the solver
+        stream; the steps advance the state)."""
+        ms = (C.c_double * 6)()
+        nl = (C.c_int * 2)()
+        self._c(self._L.hlf_time_launches(self._h, steps, first_step, ms, nl))
+        return {"vel": [ms[i] for i in range(nl[0])], "pre": [ms[3 + i] for i in range(nl[1])]}
+
+    def path_counters(self) -> dict:
+        a = (C.c_int64 * 6)()
+        self._c(self._L.hlf_read_path_counters(self._h, a))
+        out = {}
+        for i, kind in enumerate(("vel", "pre")):
+            out[kind] = {"ctas": a[3 * i], "tma_rows": a[3 * i + 1], "tma_targets": a[3 * i + 2]}
+        return out
 
     @property
     def launch_count(self) -> int:

@@ -16,7 +16,8 @@ def pytest_configure(config):
 
 def _ensure_oracle():
     so = os.path.join(ROOT, "oracle", "_build", "libhlf_oracle.so")
-    if not os.path.exists(so):
+    fma = os.path.join(ROOT, "oracle", "_build", "libhlf_oracle_fma.so")
+    if not os.path.exists(so) or not os.path.exists(fma):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "oracle"], check=True)
     ref = os.path.join(ROOT, "oracle", "_ref", "libhlf_refc.so")
     if not os.path.exists(ref) and os.path.isdir("/root/reference/proj/src"):

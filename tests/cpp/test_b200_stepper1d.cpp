@@ -169,6 +169,53 @@ TEST_CASE("running past the stability limit raises an instability error") {
   CHECK(blew_up);
 }
 
+TEST_CASE("after an instability a re-initialised state steps cleanly") {
+  // check_finite (stepper1d.cpp:121-129) looks at the current state only:
+  // the same stepper object must not report a stale step afterwards
+  Problem1d prob = standing_wave_problem();
+  Grid1d g = Grid1d::over(-1.0, 1.0, 16);
+  DeviceStepper1d stepper(prob, g, 2);
+  SchemeConfig cfg;
+  cfg.m = 2;
+  cfg.cfl = 2.5;
+  State1d st = stepper.init_leapfrog(cfg.dt_nominal_1d(g.h, prob.c_max));
+  CHECK_THROWS_AS(stepper.advance_n(st, 5000, 0), InstabilityError);
+  cfg.cfl = 0.5;
+  State1d ok = stepper.init_leapfrog(cfg.dt_nominal_1d(g.h, prob.c_max));
+  CHECK_NOTHROW(stepper.advance_n(ok, 20, 0));
+  CHECK_NOTHROW(stepper.step_system(ok, 20));
+  for (const Jet& j : ok.p) CHECK(std::isfinite(j[0]));
+}
+
+TEST_CASE("advance_to is the caller loop of leapfrog_l2") {
+  // tests/test_stepper1d.cpp:29-41 with the loop replaced by advance_to
+  Problem1d prob = standing_wave_problem();
+  for (int K : {10, 20, 40}) {
+    Grid1d g = Grid1d::over(prob.x_min, prob.x_max, K);
+    SchemeConfig cfg;
+    cfg.m = 2;
+    cfg.cfl = 0.9;
+    const double T = 4.13;
+    const int nsteps = step_count(T, cfg.dt_nominal_1d(g.h, prob.c_max));
+    const double dt = T / nsteps;
+    Stepper1d ref(prob, g, 2);
+    State1d rst = ref.init_leapfrog(dt);
+    for (int i = 0; i < nsteps; ++i) ref.step_system(rst, i);
+    DeviceStepper1d dev(prob, g, 2);
+    State1d st = dev.init_leapfrog(dt);
+    CHECK(dev.advance_to(st, T) == nsteps);
+    CHECK(st.t_p == rst.t_p);
+    CHECK(st.t_v == rst.t_v);
+    for (int j = 0; j < K; ++j)
+      for (int s = 0; s <= 2; ++s) {
+        CHECK(st.p[j][s] == doctest::Approx(rst.p[j][s]).epsilon(1e-12));
+        CHECK(st.v[j][s] == doctest::Approx(rst.v[j][s]).epsilon(1e-12));
+      }
+    State1d bad = dev.init_leapfrog(dt);
+    CHECK_THROWS_AS(dev.advance_to(bad, T + 0.5 * dt), ConfigError);
+  }
+}
+
 TEST_CASE("standing wave convergence, Hermite-leapfrog") {
   // tests/test_stepper1d.cpp:323-339 (values pinned to 5 digits there)
   Problem1d prob = standing_wave_problem();

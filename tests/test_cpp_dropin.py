@@ -1,5 +1,7 @@
-"""The C++ drop-in (include/hlf/b200/stepper1d.hpp) driven by the reference's
-own Stepper1d test cases (tests/cpp/test_b200_stepper1d.cpp), on the GPU."""
+"""The C++ drop-ins (include/hlf/b200/stepper1d.hpp, stepper2d.hpp) driven by
+the reference's own Stepper1d test cases (tests/cpp/test_b200_stepper1d.cpp)
+and by the stepper2d module's checks over the reference's 2D types
+(tests/cpp/test_b200_stepper2d.cpp), on the GPU."""
 import os
 import subprocess
 
@@ -8,6 +10,7 @@ import pytest
 import oracle as O
 
 EXE = os.path.join(O.HERE, "_ref", "test_b200_stepper1d")
+EXE2D = os.path.join(O.HERE, "_ref", "test_b200_stepper2d")
 
 
 @pytest.mark.gpu
@@ -25,3 +28,13 @@ def test_cpp_dropin_rejects_unsupported_features_without_gpu():
         pytest.skip("drop-in test binary not built")
     r = subprocess.run([EXE], capture_output=True, text=True, timeout=600)
     assert "unsupported problem features" not in r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_stepper2d_suite():
+    if not os.path.exists(EXE2D):
+        pytest.skip("2D drop-in test binary not built (needs /root/reference at build time)")
+    r = subprocess.run([EXE2D], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "| 0 failed" in r.stdout

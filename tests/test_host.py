@@ -3,12 +3,14 @@ library loads and exports every entry point include/hlf_b200.h declares, the
 host operator builder matches the reference, and configuration errors follow
 the reference's exception mapping (no compute without a GPU)."""
 import ctypes
+import math
 import os
 import re
 
 import numpy as np
 import pytest
 
+import oracle as O
 import paper_1808_10481_b200 as H
 from paper_1808_10481_b200 import _lib
 
@@ -133,3 +135,20 @@ def test_missing_extension_fails_loudly(tmp_path):
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
     assert r.returncode != 0
     assert "absent.so" in r.stderr and "missing" in r.stderr
+
+
+@pytest.mark.parametrize("T,dtn", [(1.0, 0.9 * 2.0 / 256), (4.13, 0.9 * 2.0 / 20), (3.2, 0.07), (0.5, 0.5)])
+def test_plan_steps_is_the_reference_caller_rule(T, dtn):
+    # step_count (config.cpp:34-38) and dt = T / n (tests/test_stepper1d.cpp:33-35)
+    n, dt = H.plan_steps(T, dtn)
+    assert n == math.ceil(T / dtn)
+    assert dt == T / n
+    if O.ref_available():
+        assert n == O.ref_step_count(T, dtn)
+
+
+def test_plan_steps_guards():
+    with pytest.raises(H.ConfigError):
+        H.plan_steps(0.0, 0.1)
+    with pytest.raises(H.ConfigError):
+        H.plan_steps(1.0, -0.1)
