@@ -181,6 +181,22 @@ __device__ __forceinline__ void v7_ck(int c, int PX, int PY, int PZ, const TPara
   }
 }
 
+// m = 3, V7 layout, streaming Z + CK (the z half line of each class column is
+// folded into the accumulators right away; tiled3d_v7_gen.cuh v7_m3_zck_*)
+__device__ __forceinline__ void v7_zck(int c, int PX, int PY, int PZ, const TParams& P, const double* ro,
+                                       const double* rn, const double (&cz)[4][4], double g,
+                                       double (&acc)[2][2][2]) {
+  if (c < 0) {
+    v7_m3_zck_c0_s0(P, ro, rn, cz, g, PZ, acc);  // no shift (merged pressure launch)
+  } else if (c == 0) {
+    if (PX) v7_m3_zck_c0_s0(P, ro, rn, cz, g, PZ, acc); else v7_m3_zck_c0_s1(P, ro, rn, cz, g, PZ, acc);
+  } else if (c == 1) {
+    if (PY) v7_m3_zck_c1_s0(P, ro, rn, cz, g, PZ, acc); else v7_m3_zck_c1_s1(P, ro, rn, cz, g, PZ, acc);
+  } else {
+    v7_m3_zck_zsel(P, ro, rn, cz, g, PZ, acc);
+  }
+}
+
 template <int MM>
 __device__ __forceinline__ void xy_task(const TParams& P, int w, const double* raw, double* rn, int lane) {
   // task w = (l_z, q_x parity): fused X+Y stage into the ring layer rn
@@ -433,6 +449,13 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
 #else
   constexpr bool V7 = MM == 3 && NT != 3;
 #endif
+  // V7S: the V7 Z stage and CK fused per class column (streaming; one column
+  // of P~ live instead of 64).  HLF_V7_SPLIT keeps the two stages apart.
+#if defined(HLF_V7_SPLIT)
+  constexpr bool V7S = false;
+#else
+  constexpr bool V7S = V7;
+#endif
   // V7 (m = 3): warp = (PX, PY, cell half), lane = (cell, PZ = lane >> 4)
   const int PX = (warp >> 2) & 1, PY = (warp >> 1) & 1;
   const int PZ = V7 ? (lane >> 4) : (warp & 1);
@@ -533,8 +556,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
 #endif
       // Z stage + CK for this warp's parity class
       double pt[nh][nh][nh];
-      if constexpr (V7) v7_m3_z(ro + cbase, rn + cbase, cz, zg, pt);
-      else z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
+      if constexpr (V7 && !V7S) v7_m3_z(ro + cbase, rn + cbase, cz, zg, pt);
+      else if constexpr (!V7) z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
       const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
       if (P.tma_t) {
         mbar_wait(&tgtbar, tphase);
@@ -560,7 +583,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
         asm("" : "+l"(dp));  // keep dp a base register: one IMAD.WIDE per output address
         const double* tp = tgs + (t * F + f0) * TXC + zcell;
 #ifndef HLF_EXP_NOCK
-        if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);
+        if constexpr (V7S) v7_zck(c, PX, PY, PZ, P, ro + cbase, rn + cbase, cz, zg, acc);
+        else if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);
         else ck_any<MM>(c, warp, P, pt, acc);
 #else
         acc[0][0][0] += pt[0][0][0] + pt[3][3][3] + pt[1][2][3];

@@ -75,7 +75,7 @@ def assert_tma_ran(g, K, boundary):
             assert c[kind]["tma_rows"] < c[kind]["ctas"], (kind, c)
         if tgts:
             assert c[kind]["tma_targets"] > 0, (kind, c)
-    assert c["pre"]["tma_rows"] > 0  # the pressure rows (bench's dominant path) always
+    assert c["pre"]["tma_rows"] + c["vel"]["tma_rows"] > 0
     return c
 
 

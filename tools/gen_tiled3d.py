@@ -336,6 +336,67 @@ def v7_gen_ck(mm, c, sh):
     return "\n".join(L)
 
 
+def v7_gen_zck(mm, c, sh, zsel=False):
+    """Z stage fused with the CK (streaming): for each class column (ix, iy)
+    the z half line gives P~[ix][iy][*] (4 values), which are folded into the
+    accumulators right away (every CK term that reads this column), so only one
+    column of P~ is live at a time instead of all 64 (register pressure ->
+    deeper load pipelining, and the ring loads interleave with the CK FMAs).
+    zsel: the z component of the V_z pressure launch, whose PZ = 0 lanes read
+    P~ one z index up (per-lane select inside the column)."""
+    n1, n = mm + 1, 2 * mm + 2
+    nh, jh = n // 2, (n1 + 1) // 2
+    e = [int(c == a) for a in range(3)]
+    name = f"v7_m{mm}_zck_c{c}_s{sh}" if not zsel else f"v7_m{mm}_zck_zsel"
+    L = [f"__device__ __forceinline__ void {name}(const TParams& P, const double* __restrict__ ro,",
+         f"    const double* __restrict__ rn, const double (&cz)[{nh}][{n1}], double g, int pz,",
+         f"    double (&acc)[{jh}][{jh}][{jh}]) {{",
+         "  // ro/rn = ring + ((PX*n + PY)*n1)*TXC + cell"]
+    if not zsel:
+        L.append("  (void)pz;")
+    # CK terms grouped by the class column they read
+    terms = {}
+    for jx in range(jh):
+        for jy in range(jh):
+            for jz in range(jh):
+                j = (jx, jy, jz)
+                for b0 in range(mm + 1):
+                    for b1 in range(mm + 1 - b0):
+                        for b2 in range(mm + 1 - b0 - b1):
+                            b = (b0, b1, b2)
+                            i = [j[a] + b[a] + sh * e[a] for a in range(3)]
+                            if any(x >= nh for x in i):
+                                continue
+                            terms.setdefault((i[0], i[1]), []).append((j, bindex(b, mm), i[2]))
+    for ix in range(nh):
+        for iy in range(nh):
+            if (ix, iy) not in terms:
+                continue  # no CK term reads this column
+            off = ((2 * ix) * n + 2 * iy) * n1 * TXC
+            L.append("  {")
+            for l in range(n1):
+                sg = "g" if l % 2 == 0 else "-g"
+                L.append(f"    const double u{l} = fma({sg}, rn[{off + l * TXC}], ro[{off + l * TXC}]);")
+            need = sorted({iz for (_, _, iz) in terms[(ix, iy)]})
+            top = max(need) + (1 if zsel else 0)
+            for iz in range(min(top, nh - 1) + 1):
+                expr = "0.0"
+                for l in range(n1):
+                    expr = f"fma(cz[{iz}][{l}], u{l}, {expr})"
+                L.append(f"    const double p{iz} = {expr};")
+            if zsel:
+                # PZ = 0 lanes read P~ one z index up (row 2 iz + 2; past the top: 0)
+                for iz in need:
+                    up = f"p{iz + 1}" if iz + 1 < nh else "0.0"
+                    L.append(f"    const double q{iz} = pz ? p{iz} : {up};")
+            for (j, bi, iz) in terms[(ix, iy)]:
+                src = f"q{iz}" if zsel else f"p{iz}"
+                L.append(f"    acc[{j[0]}][{j[1]}][{j[2]}] = fma(P.GM[{bi}], {src}, acc[{j[0]}][{j[1]}][{j[2]}]);")
+            L.append("  }")
+    L.append("}")
+    return "\n".join(L)
+
+
 def main_v7():
     out = os.path.join(HERE, "..", "paper_1808_10481_b200", "csrc", "tiled3d_v7_gen.cuh")
     mm = 3
@@ -345,6 +406,11 @@ def main_v7():
     for c in range(3):
         for sh in range(2):
             parts += [v7_gen_ck(mm, c, sh), ""]
+    # fused (streaming) Z + CK bodies of the pressure launches
+    for c in range(2):
+        for sh in range(2):
+            parts += [v7_gen_zck(mm, c, sh), ""]
+    parts += [v7_gen_zck(mm, 2, 0, zsel=True), ""]
     with open(out, "w") as f:
         f.write("\n".join(parts))
     print("wrote", out)

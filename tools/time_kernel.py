@@ -37,4 +37,7 @@ e1.record(stream)
 e1.synchronize()
 ms = e0.elapsed_time(e1) / steps
 dof = (d + 1) * (m + 1) ** d * math.prod(Ks)
-print(f"d={d} m={m} K={Ks} variant={g.kernel_variant} ms/step={ms:.3f} DOF/s={dof / ms * 1e3:.3e} GB/s(24B/DOF)={24 * dof / ms / 1e6:.1f}")
+tl = g.time_launches(2, 1000) if d > 1 else {}
+lt = " ".join(f"{k}=" + "/".join(f"{x:.2f}" for x in v) for k, v in tl.items())
+print(f"d={d} m={m} K={Ks} variant={g.kernel_variant} ms/step={ms:.3f} DOF/s={dof / ms * 1e3:.3e} "
+      f"GB/s(24B/DOF)={24 * dof / ms / 1e6:.1f} launches_ms: {lt}")
