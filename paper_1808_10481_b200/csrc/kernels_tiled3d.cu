@@ -340,12 +340,31 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   const bool tma_rows = P.tma && (P.pre ? (x0 >= 2 && x0 + TXC <= P.sNx) : (x0 + RAWX <= P.sNx)) && !xmirror &&
                         (P.pre ? x0 - 1 + TXC < P.K[0] : true) && !my0 && !my1 && yo1 == yo0 + P.sNx;
 #endif
+  // Edge CTAs whose row leaves the tensor in exactly one used node (pressure:
+  // x0 = 0, node sx = 0 wraps or mirrors; velocity: the last periodic tile,
+  // node sx = 32 wraps to 0) still load their rows as TMA boxes (the
+  // out-of-range nodes are zero-filled) and patch that one node per row from
+  // a register loaded one layer ahead (stored after the box has landed).
+  constexpr int NSRC = MX ? 2 : 1;
+  const int psx = P.pre ? 0 : TXC;
+  bool mx_psx;
+  const int xo_psx = xmap(psx, mx_psx);
+  const bool other_mirror = __syncthreads_or((mx_lane && lane != psx) || (mx_last && TXC != psx));
+#ifdef HLF_EXP_NORAW
+  const bool patch = false;
+#else
+  const bool patch = NB == 1 && !tma_rows && P.tma && !other_mirror && !my0 && !my1 && yo1 == yo0 + P.sNx &&
+                     (P.pre ? (x0 == 0 && TXC - 1 < P.K[0] && TXC <= P.sNx)
+                            : (P.bnd[0] == 0 && x0 + TXC == P.K[0] && x0 + TXC <= P.sNx));
+#endif
+  const bool box_rows = tma_rows || patch;
+  double pv = 0.0;  // this thread's patch value (row tid % ROWS of source tid / ROWS)
   if (tid == 0) {
     mbar_init(&rawbar[0], 1);
     mbar_init(&rawbar[1], 1);
     mbar_init(&tgtbar, 1);
     fence_mbar_init();
-    count_path(P.ctr, tma_rows, P.tma_t != 0);
+    count_path(P.ctr, box_rows, P.tma_t != 0);
   }
   __syncthreads();
   constexpr int ROWS = 2 * F;
@@ -357,9 +376,14 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     cp_async_commit();
     return;
 #endif
-    if (tma_rows) {
+    if (box_rows) {
       // one 4D box (34 nodes x 2 rows x F coefficients x 1 layer) per source
       const int stage = NB == 2 ? (layer & 1) : 0;
+      if (patch && tid < NSRC * ROWS) {
+        const int si = tid / ROWS, r = tid - si * ROWS;
+        const double* base = (si ? P.src2 : P.src) + static_cast<int64_t>(layer) * P.s_layer;
+        pv = __ldg(base + static_cast<int64_t>(r >> 1) * P.s_plane + ((r & 1) ? yo1 : yo0) + xo_psx);
+      }
       if (tid == 0) {
         constexpr int NS = MX ? 2 : 1;
         mbar_expect_tx(&rawbar[stage], NS * G::RAW * 8);
@@ -424,15 +448,19 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   };
   auto finish_raw = [&](int layer) {
     cp_async_wait_group1();  // this thread's raw(k+1) landed; its targets(k) may be in flight
-    if (tma_rows) {
+    if (box_rows) {
       const int stage = NB == 2 ? (layer & 1) : 0;
       mbar_wait(&rawbar[stage], (rphase >> stage) & 1);
       rphase ^= 1u << stage;
+      if (patch && tid < NSRC * ROWS) {
+        const int si = tid / ROWS, r = tid - si * ROWS;
+        rawbuf[(MX ? si : stage) * G::RAWS + r * RAWX + psx] = pv;  // after the box: no race with its zero fill
+      }
     }
     if (walls) {
       __syncthreads();
       fix_walls();
-      if (tma_rows) fence_proxy_async();  // generic writes before the next TMA refill of this stage
+      if (box_rows) fence_proxy_async();  // generic writes before the next TMA refill of this stage
     }
     __syncthreads();
   };

@@ -1,5 +1,6 @@
 """The z-slab decomposition (paper_1808_10481_b200/distributed.py) on CPU:
-world_size 2 over gloo, each rank stepping its slab with the oracle (as the
+world_size 2, 3 and 4 over gloo (3 and 4 make prev != next, so a swapped
+send / receive direction cannot pass), each rank stepping its slab with the oracle (as the
 compute backend) through the product's HaloExchanger / slab_step logic; the
 gathered result must equal a single-domain run bit for bit (SURVEY.md
 sec. 8(e)).  The GPU path uses the same exchange code with NCCL and the
@@ -18,7 +19,7 @@ import oracle as O
 from paper_1808_10481_b200.distributed import HaloExchanger, slab_step
 
 M_ORDER = 2
-K = [6, 5, 8]
+K = [6, 5, 12]  # z divisible by 2, 3 and 4
 
 
 def full_state(seed=11):
@@ -72,7 +73,7 @@ class OracleSlab:
         self.o.advance_v()
 
 
-def _worker(rank, world, port, steps, out_q):
+def _worker(rank, world, port, steps, out_q, swap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -85,6 +86,8 @@ def _worker(rank, world, port, steps, out_q):
     dt = 0.2 * h
     be.o.set_times(0.0, dt / 2, dt)
     halo = HaloExchanger(rank, world, be.views, be.pack, be.unpack)
+    if swap:  # deliberately wrong ring direction (test sensitivity)
+        halo.prev, halo.next = halo.next, halo.prev
     for i in range(steps):
         slab_step(be, halo, i)
     out_q.put((rank, [be.o.get_field(f) for f in range(4)]))
@@ -100,20 +103,21 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2])
-def test_slab_decomposition_matches_single_domain(world):
-    steps = 3
+def run_slabs(world, steps, swap=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, steps, q, swap)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=300) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # single-domain reference
+    return results
+
+
+def single_domain(steps):
     h = 2.0 / K[0]
     o = O.OracleStepper(3, M_ORDER, K, h, threads=1)
     state = full_state()
@@ -122,9 +126,26 @@ def test_slab_decomposition_matches_single_domain(world):
     dt = 0.2 * h
     o.set_times(0.0, dt / 2, dt)
     assert o.advance_n(steps) == -1
+    return [o.get_field(f) for f in range(4)]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_slab_decomposition_matches_single_domain(world):
+    steps = 3
+    results = run_slabs(world, steps)
+    ref = single_domain(steps)
     kz = K[2] // world
     for f in range(4):
-        ref = o.get_field(f)
         for r in range(world):
             got = results[r][f]
-            assert np.array_equal(got, slab_of(ref, r * kz, kz)), (f, r)
+            assert np.array_equal(got, slab_of(ref[f], r * kz, kz)), (f, r)
+
+
+def test_swapped_ring_direction_is_detected():
+    # with three ranks prev != next: exchanging with the wrong neighbour must
+    # change the result (the world = 2 test alone could not tell)
+    steps = 2
+    results = run_slabs(3, steps, swap=True)
+    ref = single_domain(steps)
+    kz = K[2] // 3
+    assert any(not np.array_equal(results[r][f], slab_of(ref[f], r * kz, kz)) for f in range(4) for r in range(3))

@@ -1,5 +1,6 @@
 """The product multi-GPU path with real torch.distributed point-to-point
-exchanges: two ranks (processes) on one GPU over gloo, each owning a z-slab
+exchanges: two, three and four ranks (processes) on one GPU over gloo (three
+and four make prev != next, so a swapped ring direction cannot pass), each owning a z-slab
 SlabStepper (the CUDA solver with z_slab = True) stepped by distributed.slab_step
 in its overlapped order (interior layers with the halo in flight, the
 boundary layer after it lands, hlf_advance_layers).  gloo needs host tensors,
@@ -19,7 +20,7 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 M_ORDER = 3
-K = [36, 4, 8]
+K = [36, 4, 12]  # z divisible by 2, 3 and 4
 
 
 def _state(seed=5):
@@ -88,10 +89,11 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("overlap", [True, False])
-def test_two_ranks_on_one_gpu_match_single_domain(overlap):
+def test_ranks_on_one_gpu_match_single_domain(world, overlap):
     import paper_1808_10481_b200 as H
-    world, steps = 2, 3
+    steps = 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

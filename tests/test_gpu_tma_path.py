@@ -71,8 +71,6 @@ def assert_tma_ran(g, K, boundary):
         assert c[kind]["ctas"] > 0, c
         if rows:
             assert c[kind]["tma_rows"] > 0, (kind, c)
-            # edge CTAs (wrap / walls / the partial tile) still take the per-node path
-            assert c[kind]["tma_rows"] < c[kind]["ctas"], (kind, c)
         if tgts:
             assert c[kind]["tma_targets"] > 0, (kind, c)
     assert c["pre"]["tma_rows"] + c["vel"]["tma_rows"] > 0
