@@ -48,7 +48,10 @@ class Stepper1d {
     SchemeConfig guard;  // stepper1d.cpp:95-97
     guard.m = m;
     guard.validate();
-    if (prob_.n_fields != 2) throw ConfigError("the staggered scheme needs a two-field system");
+    // one field (scalar advection, problem.hpp:16-17) runs only the modified
+    // scheme (step_modified's n_fields == 1 branch, stepper1d.cpp:205-209)
+    if (prob_.n_fields != 1 && prob_.n_fields != 2) throw ConfigError("the device path needs one or two fields");
+    one_field_ = prob_.n_fields == 1;
     op_ = build_interp_operator(m);  // the host operator, handed to the device unchanged
     std::vector<double> ap_prim, ap_dual;
     bool ap_const = true, av_const = true;
@@ -57,7 +60,7 @@ class Stepper1d {
       for (int on_dual = 0; on_dual < 2; ++on_dual) {
         const double x = on_dual ? grid_.dual(j) : grid_.primary(j);
         Jet ap = prob_.ap(x, grid_.h, n_);
-        Jet av = prob_.av(x, grid_.h, n_);
+        Jet av = one_field_ ? constant_jet(0.0, n_) : prob_.av(x, grid_.h, n_);
         if (j == 0 && on_dual == 0) {
           ap0 = ap[0];
           av0 = av[0];
@@ -90,8 +93,11 @@ class Stepper1d {
     ap_const_ = ap_const;
   }
 
+  bool one_field() const { return one_field_; }
+
   // stepper1d.cpp:131-145
   State1d init_leapfrog(double dt, double t0 = 0.0) const {
+    if (one_field_) throw ConfigError("init_leapfrog requires a two-field system");  // stepper1d.cpp:132-133
     State1d st;
     st.dt = dt;
     st.t_p = t0;
@@ -171,6 +177,22 @@ class Stepper1d {
     return st;
   }
   void step_modified(ModifiedState1d& st, int step_index) const {
+    if (one_field_) {
+      // device fields: 0 = u primary (t), 1 = u dual (t + dt/2)
+      DeviceStepper& dev = alt(HLF_SCHEME_MODIFIED_ADVECTION);
+      dev.set_field(0, flat(st.prim[0]));
+      dev.set_field(1, flat(st.dual[0]));
+      dev.set_times(st.t, st.t + st.dt / 2.0, st.dt);
+      auto down = [&] {
+        unflat(dev.get_field(0), st.prim[0]);
+        unflat(dev.get_field(1), st.dual[0]);
+        double tv = 0.0, dt = 0.0;
+        dev.times(st.t, tv, dt);
+      };
+      alt_guarded([&] { dev.step(step_index); }, down);
+      down();
+      return;
+    }
     DeviceStepper& dev = alt(HLF_SCHEME_MODIFIED);
     // device fields: 0 = p primary, 1 = v dual, 2 = v primary, 3 = p dual
     const std::vector<Jet>* in[4] = {&st.prim[0], &st.dual[1], &st.prim[1], &st.dual[0]};
@@ -188,6 +210,7 @@ class Stepper1d {
 
   // ---- classic two-half-step Hermite baseline (stepper1d.cpp:235-272)
   DualState1d init_dual_hermite(double dt, double t0 = 0.0) const {
+    if (one_field_) throw ConfigError("the classic Hermite baseline needs a two-field system");  // stepper1d.cpp:236-237
     DualState1d st;
     st.dt = dt;
     st.t = t0;
@@ -227,7 +250,8 @@ class Stepper1d {
   std::unique_ptr<DeviceStepper> dev_;
   hlf_desc desc_{};
   bool ap_const_ = true;
-  mutable std::unique_ptr<DeviceStepper> alt_dev_[3];  // per alternative scheme, created on first use
+  bool one_field_ = false;
+  mutable std::unique_ptr<DeviceStepper> alt_dev_[4];  // per alternative scheme, created on first use
 
   DeviceStepper& alt(int scheme) const {
     if (!ap_const_) throw ConfigError("the modified / Dual-Hermite device path needs constant coefficients");
@@ -304,6 +328,7 @@ class Stepper1d {
   }
 
   void upload(const State1d& st) const {
+    if (one_field_) throw ConfigError("the Hermite-leapfrog half steps require a two-field system");
     const int n1 = m_ + 1;
     if (static_cast<int>(st.p.size()) != grid_.K || static_cast<int>(st.v.size()) != grid_.K)
       throw std::invalid_argument("State1d must hold one jet per node");

@@ -92,6 +92,10 @@ typedef struct hlf_desc {
 #define HLF_SCHEME_LEAPFROG 0
 #define HLF_SCHEME_MODIFIED 1
 #define HLF_SCHEME_DUAL_HERMITE 2
+/* MODIFIED_ADVECTION  the single-field branch of step_modified (n_fields == 1,
+                stepper1d.cpp:205-209, ck_advection :40-52): u_t = ap u_x on both
+                grids: field 0 = u primary (t), field 1 = u dual (t + dt/2) */
+#define HLF_SCHEME_MODIFIED_ADVECTION 3
 
 /* --- interpolation operator ---------------------------------------------- */
 /* M = A^{-1} (row-major, (2m+2)^2) and its 1-norm condition; HLF_CONFIG_ERROR for m outside [0, 8] */
@@ -213,6 +217,35 @@ hlf_status hlf_energy_1d(hlf_solver* s, int kind, double c, double* energy);
    of component c (before advance_p). */
 hlf_status hlf_halo_send_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr, int64_t* count);
 hlf_status hlf_halo_recv_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr, int64_t* count);
+
+/* --- multi-GPU z slabs from one C++ host process ------------------------- */
+/* A periodic 3D domain (global desc; K[2] cells along z) split into n z slabs
+   of K[2]/n layers, slab r on devices[r]; each half step
+   exchanges one layer with the ring neighbours, overlapped with the interior
+   layers (the same arithmetic as one solver over the whole domain).
+   transport: HLF_TRANSPORT_NCCL (ncclSend/ncclRecv over an ncclCommInitAll
+   clique; one device per slab), HLF_TRANSPORT_COPY (cudaMemcpyPeerAsync; also
+   several slabs on one device), HLF_TRANSPORT_AUTO (NCCL when the devices are
+   distinct and libnccl.so.2 loads, else COPY).  The reference has no
+   multi-process or multi-GPU code; this replaces the
+   caller loop over step_system for a sharded domain. */
+typedef struct hlf_slab_group hlf_slab_group; /* opaque */
+enum { HLF_TRANSPORT_AUTO = 0, HLF_TRANSPORT_NCCL = 1, HLF_TRANSPORT_COPY = 2 };
+hlf_status hlf_slabs_create(const hlf_desc* global, int n, const int* devices, int transport, hlf_slab_group** out);
+void hlf_slabs_destroy(hlf_slab_group* g);
+const char* hlf_slabs_last_error(const hlf_slab_group* g);
+int hlf_slabs_count(const hlf_slab_group* g);
+int hlf_slabs_transport(const hlf_slab_group* g);
+/* slab r's solver (fields, accessors; AoS host data of that slab only) */
+hlf_solver* hlf_slabs_solver(hlf_slab_group* g, int r);
+hlf_status hlf_slabs_set_times(hlf_slab_group* g, double t_p, double t_v, double dt);
+/* steps indexed first_step.. on every slab; HLF_INSTABILITY with the first
+   non-finite step over all slabs */
+hlf_status hlf_slabs_advance_n(hlf_slab_group* g, int steps, int first_step);
+hlf_status hlf_slabs_synchronize(hlf_slab_group* g);
+
+/* the cudaStream_t the solver launches on (as void*) */
+void* hlf_get_stream(const hlf_solver* s);
 
 /* number of kernels this solver has launched (for launch accounting) */
 int64_t hlf_launch_count(const hlf_solver* s);

@@ -6,5 +6,5 @@ reference's solver interface (proj/include/hlf)."""
 from .solver import (  # noqa: F401
     DUAL, PERIODIC, PRIMARY, REFLECTIVE, ConfigError, CudaError, Grid, Grid1d, Grid2d, Grid3d,
     InstabilityError, InterpOperator, MaxwellTM2d, SchemeConfig, Stepper, Stepper1d, Stepper2d, Stepper3d,
-    SCHEME_DUAL_HERMITE, SCHEME_LEAPFROG, SCHEME_MODIFIED, build_interp_operator, plan_steps, step_count,
+    SCHEME_DUAL_HERMITE, SCHEME_LEAPFROG, SCHEME_MODIFIED, SCHEME_MODIFIED_ADVECTION, build_interp_operator, plan_steps, step_count,
 )

@@ -26,7 +26,9 @@ EXPORTS = [
     "hlf_poll_finite", "hlf_clear_finite", "hlf_synchronize", "hlf_field_device",
     "hlf_fill_separable", "hlf_error_separable", "hlf_zero_field", "hlf_halo_send_ptr", "hlf_halo_recv_ptr",
     "hlf_launch_count", "hlf_kernel_variant", "hlf_set_kernel_variant", "hlf_enable_path_counters",
-    "hlf_read_path_counters", "hlf_time_launches",
+    "hlf_read_path_counters", "hlf_time_launches", "hlf_slabs_create", "hlf_slabs_destroy",
+    "hlf_slabs_last_error", "hlf_slabs_count", "hlf_slabs_transport", "hlf_slabs_solver", "hlf_slabs_set_times",
+    "hlf_slabs_advance_n", "hlf_slabs_synchronize", "hlf_get_stream",
 ]
 
 
@@ -109,6 +111,16 @@ def lib() -> C.CDLL:
         "hlf_enable_path_counters": ([S, C.c_int], st),
         "hlf_read_path_counters": ([S, C.POINTER(C.c_int64)], st),
         "hlf_time_launches": ([S, C.c_int, C.c_int, _dp, C.POINTER(C.c_int)], st),
+        "hlf_slabs_create": ([C.POINTER(HlfDesc), C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)], st),
+        "hlf_slabs_destroy": ([S], None),
+        "hlf_slabs_last_error": ([S], C.c_char_p),
+        "hlf_slabs_count": ([S], C.c_int),
+        "hlf_slabs_transport": ([S], C.c_int),
+        "hlf_slabs_solver": ([S, C.c_int], C.c_void_p),
+        "hlf_slabs_set_times": ([S, C.c_double, C.c_double, C.c_double], st),
+        "hlf_slabs_advance_n": ([S, C.c_int, C.c_int], st),
+        "hlf_slabs_synchronize": ([S], st),
+        "hlf_get_stream": ([S], C.c_void_p),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

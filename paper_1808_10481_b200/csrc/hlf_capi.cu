@@ -425,7 +425,7 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
   }
   if (desc->z_slab && (d != 3 || desc->boundary[2] != HLF_PERIODIC))
     return fail(nullptr, HLF_CONFIG_ERROR, "z slabs need d = 3 with a periodic z axis");
-  if (desc->scheme < HLF_SCHEME_LEAPFROG || desc->scheme > HLF_SCHEME_DUAL_HERMITE)
+  if (desc->scheme < HLF_SCHEME_LEAPFROG || desc->scheme > HLF_SCHEME_MODIFIED_ADVECTION)
     return fail(nullptr, HLF_CONFIG_ERROR, "unknown time scheme");
   if (desc->scheme != HLF_SCHEME_LEAPFROG &&
       (d != 1 || desc->boundary[0] != HLF_PERIODIC || desc->variable_ap || desc->z_slab))
@@ -445,7 +445,7 @@ hlf_status hlf_create(const hlf_desc* desc, hlf_solver** out) {
   s->variable = desc->variable_ap != 0;
   s->z_slab = desc->z_slab != 0;
   s->scheme = desc->scheme;
-  s->nfields = desc->scheme == HLF_SCHEME_LEAPFROG ? d + 1 : 4;
+  s->nfields = desc->scheme == HLF_SCHEME_LEAPFROG ? d + 1 : (desc->scheme == HLF_SCHEME_MODIFIED_ADVECTION ? 2 : 4);
   s->device = desc->device;
   for (int ax = 0; ax < 3; ++ax) {
     const bool used = ax < d;
@@ -699,7 +699,22 @@ static hlf_status scheme1d_step(hlf_solver* s, int step_index) {
   P.step = step_index;
   P.flag = s->flag;
   int launched = 0;
-  if (s->scheme == HLF_SCHEME_MODIFIED) {
+  if (s->scheme == HLF_SCHEME_MODIFIED_ADVECTION) {
+    // the single-field branch of step_modified (stepper1d.cpp:205-209):
+    // ck_advection's recurrence U_{r+1} = a D U_r (:40-52) is the two-table
+    // recurrence with both tables seeded by the same reconstruction and
+    // av = ap (the tables stay equal level by level, value for value), so the
+    // two-field kernel runs it with the second field aliased to the first
+    P.av = s->ap;
+    P.to_primary = 1;
+    P.src_p = P.src_v = s->field[1];
+    P.dst_p = P.dst_v = s->field[0];
+    launched += hlfk::launch_modified_1d(s->m, P, s->stream);
+    P.to_primary = 0;
+    P.src_p = P.src_v = s->field[0];
+    P.dst_p = P.dst_v = s->field[1];
+    launched += hlfk::launch_modified_1d(s->m, P, s->stream);
+  } else if (s->scheme == HLF_SCHEME_MODIFIED) {
     // primary update from the dual copies, then dual update from the new primary
     P.to_primary = 1;
     P.src_p = s->field[3];
@@ -728,7 +743,7 @@ static hlf_status scheme1d_step(hlf_solver* s, int step_index) {
   s->launches += launched;
   HLF_CUDA(s, cudaGetLastError());
   s->t_p += s->dt;
-  s->t_v = s->scheme == HLF_SCHEME_MODIFIED ? s->t_p + s->dt / 2.0 : s->t_p;
+  s->t_v = s->scheme == HLF_SCHEME_DUAL_HERMITE ? s->t_p : s->t_p + s->dt / 2.0;
   return HLF_OK;
 }
 
@@ -761,7 +776,7 @@ static hlf_status reset_flag(hlf_solver* s) {
 static void advance_times(hlf_solver* s) {
   s->t_p += s->dt;
   if (s->scheme == HLF_SCHEME_LEAPFROG) s->t_v += s->dt;
-  else s->t_v = s->scheme == HLF_SCHEME_MODIFIED ? s->t_p + s->dt / 2.0 : s->t_p;
+  else s->t_v = s->scheme == HLF_SCHEME_DUAL_HERMITE ? s->t_p : s->t_p + s->dt / 2.0;
 }
 
 // capture `chunk` steps (step offsets 0..chunk-1) into s->graph_exec; on any
@@ -1134,6 +1149,7 @@ hlf_status hlf_halo_recv_ptr(hlf_solver* s, int kind, int comp, double** dev_ptr
 }
 
 int64_t hlf_launch_count(const hlf_solver* s) { return s ? s->launches : -1; }
+void* hlf_get_stream(const hlf_solver* s) { return s ? static_cast<void*>(s->stream) : nullptr; }
 
 hlf_status hlf_enable_path_counters(hlf_solver* s, int on) {
   if (!s) return HLF_INVALID_ARGUMENT;

@@ -22,7 +22,8 @@ import time
 
 import numpy as np
 
-from .solver import Grid, Stepper
+from . import _lib as _L
+from .solver import PERIODIC, ConfigError, Grid, Stepper, _check, build_interp_operator
 
 
 class _DevArray:
@@ -230,3 +231,95 @@ class SlabStepper:
                 "job": {"leapfrog_steps": steps, "h2d_bytes": nbytes, "d2h_bytes": nbytes, "seconds": sec,
                         "api": "hlf_set_field x4 (pinned host AoS) + hlf_advance_p/v_indexed x steps + "
                                "hlf_poll_finite + hlf_get_field x4, wall clock", "finite": bad < 0}}
+
+
+TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_COPY = 0, 1, 2
+
+
+class SlabGroup:
+    """The C++ host's multi-GPU path (hlf_slabs_*, csrc/hlf_slabs.cu): one
+    process drives n z-slab solvers of a periodic 3D box, slab r on
+    devices[r], with the one-layer halos of every half step exchanged by NCCL
+    (distinct devices) or peer copies (any devices, e.g. several slabs on one
+    GPU), overlapped with the interior layers.  Host data per slab use the
+    solver layout (x-major AoS [node][coef] of that slab's nodes)."""
+
+    def __init__(self, K_global, h: float, m: int, devices, transport: int = TRANSPORT_AUTO,
+                 x_min=(-1.0, -1.0, -1.0), ap: float = -1.0, av: float = -1.0):
+        L = _L.lib()
+        d = _L.HlfDesc()
+        d.dim = 3
+        d.m = m
+        for a in range(3):
+            d.K[a] = K_global[a]
+            d.x_min[a] = x_min[a]
+            d.boundary[a] = PERIODIC
+        d.h = h
+        d.ap, d.av = ap, av
+        self._M = np.ascontiguousarray(build_interp_operator(m).M, dtype=np.float64).ravel()
+        d.M = self._M.ctypes.data_as(_L._dp)
+        devs = (_L.C.c_int * len(devices))(*devices)
+        g = _L.C.c_void_p()
+        st = L.hlf_slabs_create(_L.C.byref(d), len(devices), devs, transport, _L.C.byref(g))
+        if st != _L.HLF_OK:
+            msg = L.hlf_slabs_last_error(None)
+            raise ConfigError((msg or b"").decode()) if st == _L.HLF_CONFIG_ERROR else RuntimeError(
+                f"hlf_slabs_create: status {st}: {(msg or b'').decode()}")
+        self._g, self._L = g, L
+        self.n = len(devices)
+        self.m, self.F = m, (m + 1) ** 3
+        self.K_global = tuple(K_global)
+        self.kz = K_global[2] // self.n
+
+    def close(self):
+        if getattr(self, "_g", None):
+            self._L.hlf_slabs_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def transport(self) -> int:
+        return int(self._L.hlf_slabs_transport(self._g))
+
+    def _solver(self, r: int):
+        return self._L.hlf_slabs_solver(self._g, r)
+
+    def _chk(self, st):
+        if st != _L.HLF_OK:
+            msg = (self._L.hlf_slabs_last_error(self._g) or b"").decode()
+            if st == _L.HLF_INSTABILITY:
+                from .solver import InstabilityError
+                raise InstabilityError(int(msg.rsplit(" ", 1)[-1]), msg)
+            raise RuntimeError(f"slab group: status {st}: {msg}")
+
+    def set_field(self, r: int, f: int, host):
+        a = np.ascontiguousarray(host, dtype=np.float64)
+        s = self._solver(r)
+        _check(self._L.hlf_set_field(s, f, a.ctypes.data), s)
+
+    def get_field(self, r: int, f: int):
+        s = self._solver(r)
+        grid = 0 if f == 0 else 1
+        out = np.empty((int(self._L.hlf_num_nodes(s, grid)), self.F))
+        _check(self._L.hlf_get_field(s, f, out.ctypes.data), s)
+        return out
+
+    def set_times(self, t_p, t_v, dt):
+        self._chk(self._L.hlf_slabs_set_times(self._g, t_p, t_v, dt))
+
+    def times(self, r: int = 0):
+        a, b, c = _L.C.c_double(), _L.C.c_double(), _L.C.c_double()
+        s = self._solver(r)
+        _check(self._L.hlf_get_times(s, _L.C.byref(a), _L.C.byref(b), _L.C.byref(c)), s)
+        return a.value, b.value, c.value
+
+    def advance_n(self, steps: int, first_step: int = 0):
+        self._chk(self._L.hlf_slabs_advance_n(self._g, steps, first_step))
+
+    def synchronize(self):
+        self._chk(self._L.hlf_slabs_synchronize(self._g))

@@ -84,7 +84,7 @@ def plan_steps(T: float, dt_nominal: float):
 
 
 # time schemes (hlf::Variant, config.hpp:9; hlf_b200.h HLF_SCHEME_*)
-SCHEME_LEAPFROG, SCHEME_MODIFIED, SCHEME_DUAL_HERMITE = 0, 1, 2
+SCHEME_LEAPFROG, SCHEME_MODIFIED, SCHEME_DUAL_HERMITE, SCHEME_MODIFIED_ADVECTION = 0, 1, 2, 3
 
 
 @dataclass

@@ -304,8 +304,62 @@ TEST_CASE("discrete invariants hold across steps and orders") {
 TEST_CASE("unsupported problem features are configuration errors") {
   Grid1d g = Grid1d::over(0.0, 2.0 * pi, 16);
   CHECK_THROWS_AS(DeviceStepper1d(standing_wave_problem(), g, 9), ConfigError);   // m cap
+}
+
+TEST_CASE("a one-field problem runs only the modified scheme") {
+  // the leapfrog and Dual-Hermite initialisers throw like the reference's
+  // (stepper1d.cpp:132-133, 236-237)
+  Grid1d g = Grid1d::over(0.0, 2.0 * pi, 16);
   Problem1d adv = advection_problem();
-  CHECK_THROWS_AS(DeviceStepper1d(adv, g, 2), ConfigError);                       // one field
+  DeviceStepper1d dev(adv, g, 2);
+  CHECK_THROWS_AS(dev.init_leapfrog(0.1), ConfigError);
+  CHECK_THROWS_AS(dev.init_dual_hermite(0.1), ConfigError);
+}
+
+TEST_CASE("modified scheme advection convergence (single field) on the device") {
+  // tests/test_stepper1d.cpp:357-371 (PAPER Table 3) with the device stepper:
+  // the reference's own goldens and rate band
+  Problem1d prob = advection_problem();
+  const double T = 4.13, cfl = 0.9;
+  std::vector<int> Ks = {10, 20, 40};
+  std::vector<double> expect = {1.298e-03, 2.212e-05, 3.541e-07};
+  std::vector<double> hs, es;
+  for (size_t i = 0; i < Ks.size(); ++i) {
+    Grid1d g = Grid1d::over(prob.x_min, prob.x_max, Ks[i]);
+    SchemeConfig cfg;
+    cfg.m = 2;
+    cfg.cfl = cfl;
+    const int nsteps = step_count(T, cfg.dt_nominal_1d(g.h, prob.c_max));
+    const double dt = T / nsteps;
+    DeviceStepper1d stepper(prob, g, 2);
+    ModifiedState1d st = stepper.init_modified(dt);
+    for (int k = 0; k < nsteps; ++k) stepper.step_modified(st, k);
+    const double e = l2_error_1d(st.prim[0], g, stepper.op(), true,
+                                 [&](double x) { return prob.exact_value(0, x, st.t); });
+    CHECK(e == doctest::Approx(expect[i]).epsilon(0.02));
+    hs.push_back(2.0 / Ks[i]);
+    es.push_back(e);
+  }
+  RateFit fit = convergence_rate(hs, es);
+  CHECK(std::abs(fit.rate - 5.98) < 0.4);
+}
+
+TEST_CASE("single-field modified scheme matches the reference bit for bit") {
+  Problem1d prob = advection_problem();
+  for (int m = 0; m <= 5; ++m) {
+    Grid1d g = Grid1d::over(prob.x_min, prob.x_max, 24);
+    Stepper1d ref(prob, g, m);
+    DeviceStepper1d dev(prob, g, m);
+    const double dt = 0.4 * g.h / prob.c_max;
+    ModifiedState1d a = ref.init_modified(dt), b = dev.init_modified(dt);
+    for (int i = 0; i < 30; ++i) {
+      ref.step_modified(a, i);
+      dev.step_modified(b, i);
+    }
+    CHECK(max_rel(b.prim[0], a.prim[0]) == 0.0);
+    CHECK(max_rel(b.dual[0], a.dual[0]) == 0.0);
+    CHECK(b.t == a.t);
+  }
 }
 
 TEST_CASE("modified and Dual-Hermite variants match the reference bit for bit") {
