@@ -719,6 +719,8 @@ int launch_one(TParams T, cudaStream_t st) {
   const size_t smem = sizeof(double) * G::template SMEM_DOUBLES<NT> + 128;
   static std::atomic<unsigned long long> configured{0};
   ensure_smem_opt_in(tiled3d<MM, NT>, static_cast<int>(smem), configured);
+  // x-fastest rasterisation; y-fastest (neighbouring rows, which share a
+  // source row, launched side by side) measured 1 % slower at 512x512x256
   dim3 grid((T.tNx + TXC - 1) / TXC, T.tNy, (T.tNz + ZC - 1) / ZC);
   tiled3d<MM, NT><<<grid, NTHREADS, smem, st>>>(T);
   mark_launch(*T.hp, st);
