@@ -118,6 +118,15 @@ hlf_status hlf_set_field(hlf_solver* s, int field, const double* host_aos);
 hlf_status hlf_get_field(hlf_solver* s, int field, double* host_aos);
 /* per-node ap jets, (2m+2)^d entries per node (x-major), for grid HLF_PRIMARY / HLF_DUAL */
 hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets);
+/* ap = -(c0 + c1 prod_ax sin(w[ax] x_ax + phase[ax])) at every node of both
+   grids (ap = -c^2 with a separable c^2, e.g. the SURVEY.md sec. 8(d) config 3
+   speed c^2 = 1 + sin(pi x) sin(pi y) / 2 and its 3D extension); av stays the
+   scalar desc.av.  Replaces hlf_set_coeff for this family: the jets are the
+   reference's scaled sin jets (sin_jet, jet.cpp:65-74) in outer product.  In
+   3D with m <= 3 they are generated inside the kernel (var3d: no stored
+   coefficient grids, 24 B per DOF-update); otherwise they are written to the
+   per-node jet storage on the device.  Needs desc.variable_ap = 1. */
+hlf_status hlf_set_coeff_separable(hlf_solver* s, double c0, double c1, const double* w, const double* phase);
 /* 1D forcing (ck_recurrence_variable's z, stepper1d.cpp:22-38): the table for
    the NEXT half step that updates `grid` (HLF_PRIMARY: hlf_advance_p, evaluated
    by the reference at (primary x_j, t_v); HLF_DUAL: hlf_advance_v, at (dual x_j,

@@ -19,7 +19,7 @@ HLF_NCCL_ERROR = 5
 # every exported symbol declared in include/hlf_b200.h
 EXPORTS = [
     "hlf_abi_version", "hlf_build_interp_operator", "hlf_create", "hlf_destroy", "hlf_last_error",
-    "hlf_num_nodes", "hlf_num_coeffs", "hlf_set_field", "hlf_get_field", "hlf_set_coeff",
+    "hlf_num_nodes", "hlf_num_coeffs", "hlf_set_field", "hlf_get_field", "hlf_set_coeff", "hlf_set_coeff_separable",
     "hlf_set_forcing", "hlf_clear_forcing", "hlf_set_graph_steps", "hlf_l2_error_separable", "hlf_energy_1d",
     "hlf_set_times", "hlf_get_times", "hlf_set_dt", "hlf_advance_p", "hlf_advance_v", "hlf_step",
     "hlf_advance_n", "hlf_plan_steps", "hlf_advance_to", "hlf_advance_p_indexed", "hlf_advance_v_indexed", "hlf_advance_layers", "hlf_commit_half",
@@ -77,6 +77,7 @@ def lib() -> C.CDLL:
         "hlf_set_field": ([S, C.c_int, C.c_void_p], st),
         "hlf_get_field": ([S, C.c_int, C.c_void_p], st),
         "hlf_set_coeff": ([S, C.c_int, C.c_void_p], st),
+        "hlf_set_coeff_separable": ([S, C.c_double, C.c_double, _dp, _dp], st),
         "hlf_set_forcing": ([S, C.c_int, C.c_void_p], st),
         "hlf_set_graph_steps": ([S, C.c_int], st),
         "hlf_clear_forcing": ([S], st),

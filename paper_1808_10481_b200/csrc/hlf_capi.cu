@@ -50,6 +50,11 @@ struct hlf_solver {
   int layers[4] = {1, 1, 1, 1};
   int64_t plane[4] = {1, 1, 1, 1};
   double* coeff[2] = {nullptr, nullptr};
+  // hlf_set_coeff_separable: ap = -(c0 + c1 prod sin(w x + ph)); 3D m <= 3
+  // generates the jets inside the var3d kernel (no stored grids)
+  bool sep3d = false;
+  double sep[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // c0, c1, w[3], phase[3]
+  bool coeff_ready(int grid) const { return coeff[grid] != nullptr || sep3d; }
   double* force[2] = {nullptr, nullptr};  // 1D forcing tables [(r n + s)][x] per target grid
   bool force_on = false;
   bool force_fresh[2] = {false, false};
@@ -300,7 +305,7 @@ void fill_weights(const hlf_solver* s, hlfk::HalfKind kind, HalfParams& P) {
 // var2d (2D with per-node ap jets)
 bool tiled_available(const hlf_solver* s) {
   if (!s->m_mirror) return false;
-  if (s->variable) return s->d == 2 && hlfk::var2d_supported(s->m);
+  if (s->variable) return (s->d == 2 && hlfk::var2d_supported(s->m)) || (s->d == 3 && s->sep3d);
   return (s->d == 3 && hlfk::tiled3d_supported(s->m)) || (s->d == 2 && hlfk::tiled2d_supported(s->m));
 }
 
@@ -365,12 +370,20 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
     P.tNz = zhi - zlo;
   }
   int launched = -1;
-  if (s->variant == 1 && !s->variable && s->d == 3 && hlfk::tiled3d_supported(s->m))
+  if (s->variant == 1 && s->variable && s->sep3d && s->d == 3) {
+    // coordinates of target node 0 (primary: x_min, dual: x_min + h/2; z from the layer range)
+    double x0[3];
+    for (int ax = 0; ax < 3; ++ax) x0[ax] = s->x_min[ax] + (fg == HLF_DUAL ? 0.5 * s->h : 0.0);
+    x0[2] += zlo * s->h;
+    launched = hlfk::launch_half_var3d(s->m, kind, P, s->sep, x0, s->stream);
+  } else if (s->variant == 1 && !s->variable && s->d == 3 && hlfk::tiled3d_supported(s->m))
     launched = hlfk::launch_half_tiled3d(s->m, kind, P, s->stream);
   else if (s->variant == 1 && !s->variable && s->d == 2 && hlfk::tiled2d_supported(s->m))
     launched = hlfk::launch_half_tiled2d(s->m, kind, P, s->stream);
   else if (s->variant == 1 && s->variable && s->d == 2 && hlfk::var2d_supported(s->m))
     launched = hlfk::launch_half_var2d(s->m, kind, P, s->stream);
+  if (launched < 0 && s->variable && s->sep3d)
+    return fail(s, HLF_CONFIG_ERROR, "on-the-fly separable coefficients need the var3d kernel (variant 1, m <= 3)");
   if (launched == -2 || launched < 0 && s->variant != 1)  // -2: custom M / planes too large for the tiled kernel
     launched = hlfk::launch_half_generic(s->d, s->m, s->variable, kind, P, s->stream);
   if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
@@ -575,6 +588,39 @@ hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets) {
   return transfer(s, s->coeff[grid], N, s->E, plane * s->E, 0, const_cast<double*>(host_jets), true);
 }
 
+hlf_status hlf_set_coeff_separable(hlf_solver* s, double c0, double c1, const double* w, const double* phase) {
+  if (!s || !w || !phase) return HLF_INVALID_ARGUMENT;
+  if (!s->variable) return fail(s, HLF_CONFIG_ERROR, "solver was created with constant coefficients");
+  if (s->scheme != HLF_SCHEME_LEAPFROG) return fail(s, HLF_CONFIG_ERROR, "variable coefficients: leapfrog scheme only");
+  cudaSetDevice(s->device);
+  s->sep[0] = c0;
+  s->sep[1] = c1;
+  for (int a = 0; a < 3; ++a) {
+    s->sep[2 + a] = a < s->d ? w[a] : 0.0;
+    s->sep[5 + a] = a < s->d ? phase[a] : 0.0;
+  }
+  ++s->gen;
+  if (s->d == 3 && hlfk::var3d_supported(s->m) && s->m_mirror) {
+    s->sep3d = true;  // generated inside the kernel: nothing stored
+    s->variant = 1;   // the var3d kernel (the generic kernel reads stored jets)
+    return HLF_OK;
+  }
+  s->sep3d = false;
+  // other (d, m): expand into the stored per-node jets the var2d / generic kernels read
+  for (int grid = 0; grid < 2; ++grid) {
+    const int* N = grid == HLF_PRIMARY ? s->Np : s->Nd;
+    if (!s->coeff[grid]) {
+      const size_t bytes = static_cast<size_t>(s->num_nodes(grid)) * s->E * sizeof(double);
+      HLF_CUDA(s, cudaMalloc(&s->coeff[grid], bytes));
+    }
+    double x0[3];
+    for (int a = 0; a < 3; ++a) x0[a] = s->x_min[a] + (grid == HLF_DUAL ? 0.5 * s->h : 0.0);
+    hlfk::launch_fill_sep_coeff(s->coeff[grid], s->d, N, s->n, s->h, x0, s->sep, s->stream);
+    HLF_CUDA(s, cudaGetLastError());
+  }
+  return HLF_OK;
+}
+
 hlf_status hlf_set_forcing(hlf_solver* s, int grid, const double* host_table) {
   if (!s || (grid != HLF_PRIMARY && grid != HLF_DUAL) || !host_table)
     return fail(s, HLF_INVALID_ARGUMENT, "bad grid or buffer");
@@ -626,7 +672,7 @@ hlf_status hlf_set_dt(hlf_solver* s, double dt) {
 
 hlf_status hlf_advance_p(hlf_solver* s) {
   if (!s) return HLF_INVALID_ARGUMENT;
-  if (s->variable && !s->coeff[HLF_PRIMARY]) return fail(s, HLF_CONFIG_ERROR, "primary-grid ap jets not set");
+  if (s->variable && !s->coeff_ready(HLF_PRIMARY)) return fail(s, HLF_CONFIG_ERROR, "primary-grid ap jets not set");
   cudaSetDevice(s->device);
   hlf_status st = launch_half(s, hlfk::PRE, -1);
   if (st != HLF_OK) return st;
@@ -636,7 +682,7 @@ hlf_status hlf_advance_p(hlf_solver* s) {
 
 hlf_status hlf_advance_v(hlf_solver* s) {
   if (!s) return HLF_INVALID_ARGUMENT;
-  if (s->variable && !s->coeff[HLF_DUAL]) return fail(s, HLF_CONFIG_ERROR, "dual-grid ap jets not set");
+  if (s->variable && !s->coeff_ready(HLF_DUAL)) return fail(s, HLF_CONFIG_ERROR, "dual-grid ap jets not set");
   cudaSetDevice(s->device);
   hlf_status st = launch_half(s, hlfk::VEL, -1);
   if (st != HLF_OK) return st;
@@ -646,7 +692,7 @@ hlf_status hlf_advance_v(hlf_solver* s) {
 
 hlf_status hlf_advance_p_indexed(hlf_solver* s, int step_index) {
   if (!s) return HLF_INVALID_ARGUMENT;
-  if (s->variable && !s->coeff[HLF_PRIMARY]) return fail(s, HLF_CONFIG_ERROR, "primary-grid ap jets not set");
+  if (s->variable && !s->coeff_ready(HLF_PRIMARY)) return fail(s, HLF_CONFIG_ERROR, "primary-grid ap jets not set");
   cudaSetDevice(s->device);
   hlf_status st = launch_half(s, hlfk::PRE, step_index);
   if (st != HLF_OK) return st;
@@ -656,7 +702,7 @@ hlf_status hlf_advance_p_indexed(hlf_solver* s, int step_index) {
 
 hlf_status hlf_advance_v_indexed(hlf_solver* s, int step_index) {
   if (!s) return HLF_INVALID_ARGUMENT;
-  if (s->variable && !s->coeff[HLF_DUAL]) return fail(s, HLF_CONFIG_ERROR, "dual-grid ap jets not set");
+  if (s->variable && !s->coeff_ready(HLF_DUAL)) return fail(s, HLF_CONFIG_ERROR, "dual-grid ap jets not set");
   cudaSetDevice(s->device);
   hlf_status st = launch_half(s, hlfk::VEL, step_index);
   if (st != HLF_OK) return st;
@@ -667,7 +713,7 @@ hlf_status hlf_advance_v_indexed(hlf_solver* s, int step_index) {
 hlf_status hlf_advance_layers(hlf_solver* s, int half, int step_index, int z_begin, int z_end) {
   if (!s) return HLF_INVALID_ARGUMENT;
   if (half != 0 && half != 1) return fail(s, HLF_INVALID_ARGUMENT, "half must be 0 (pressure) or 1 (velocity)");
-  if (s->variable && !s->coeff[half == 0 ? HLF_PRIMARY : HLF_DUAL])
+  if (s->variable && !s->coeff_ready(half == 0 ? HLF_PRIMARY : HLF_DUAL))
     return fail(s, HLF_CONFIG_ERROR, "ap jets not set");
   cudaSetDevice(s->device);
   return launch_half(s, half == 0 ? hlfk::PRE : hlfk::VEL, step_index, z_begin, z_end);
@@ -749,7 +795,7 @@ static hlf_status scheme1d_step(hlf_solver* s, int step_index) {
 
 static hlf_status step_async(hlf_solver* s, int step_index) {
   if (s->scheme != HLF_SCHEME_LEAPFROG) return scheme1d_step(s, step_index);
-  if (s->variable && (!s->coeff[0] || !s->coeff[1])) return fail(s, HLF_CONFIG_ERROR, "ap jets not set");
+  if (s->variable && (!s->coeff_ready(0) || !s->coeff_ready(1))) return fail(s, HLF_CONFIG_ERROR, "ap jets not set");
   hlf_status st = launch_half(s, hlfk::PRE, step_index);
   if (st != HLF_OK) return st;
   s->t_p += s->dt;

@@ -161,6 +161,14 @@ int launch_half_tiled3d(int m, HalfKind kind, const HalfParams& p, cudaStream_t 
 bool tiled3d_supported(int m);
 int launch_half_tiled2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
 bool tiled2d_supported(int m);
+// 3D with ap = -(c0 + c1 prod sin(w x + ph)) generated on the fly, m = 1..3;
+// sep = {c0, c1, w[3], phase[3]}, x0 = coordinates of target node 0
+int launch_half_var3d(int m, HalfKind kind, const HalfParams& p, const double* sep, const double* x0,
+                      cudaStream_t st);
+bool var3d_supported(int m);
+// the same coefficient as stored per-node jets ([z][E][y][x]) of one grid
+int launch_fill_sep_coeff(double* dst, int d, const int* N, int n, double h, const double* x0, const double* sep,
+                          cudaStream_t st);
 // 2D with per-node ap jets (variable c^2), m = 1..4
 int launch_half_var2d(int m, HalfKind kind, const HalfParams& p, cudaStream_t st);
 bool var2d_supported(int m);

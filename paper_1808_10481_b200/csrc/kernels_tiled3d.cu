@@ -59,18 +59,33 @@ struct Cfg {
   template <int NT>
   static constexpr int NTGT = NT == 2 ? 1 : NT;
   template <int NT>
-  static constexpr int NRAW = NT == 2 ? 2 : ((NT == 1 && MM == 1) ? 2 : 1);
+  static constexpr int NSRC = NT == 2 ? 2 : 1;  // raw sources per stage
   template <int NT>
   static constexpr int TGT = NTGT<NT> * F * TXC;
-  // NT == 1 (pressure), m = 1: the raw stage is double-buffered so the source
-  // layer gets a whole iteration to land (+11 % at m = 1 with TMA loads; at
-  // m = 2 a single stage is 1.7 % faster, at m = 3 there is no room for it).  Targets are single-buffered: every
-  // staged target value is read by exactly one lane, which reloads its slots
-  // for the next layer right after its epilogue (no barrier needed).
+  // Raw stages (RST) and target stages (TST): the TMA box of a source layer
+  // is issued RST - 1/2 iterations and that of a target layer TST - 1
+  // iterations ahead of use.  At m = 1 an iteration is short against the DRAM
+  // round trip (the loads, not the arithmetic, set the pace), so the stages
+  // are deep; at m = 3 there is no room for a second stage (and an iteration
+  // covers the latency).  HLF_M1_RST / _TST, HLF_M2_RST / _TST override.
+#ifndef HLF_M1_RST
+#define HLF_M1_RST 4
+#endif
+#ifndef HLF_M1_TST
+#define HLF_M1_TST 3
+#endif
+#ifndef HLF_M2_RST
+#define HLF_M2_RST 1
+#endif
+#ifndef HLF_M2_TST
+#define HLF_M2_TST 1
+#endif
   template <int NT>
-  static constexpr int NBUF = (NT == 1 && MM == 1) ? 2 : 1;
+  static constexpr int RST = MM == 1 ? HLF_M1_RST : (MM == 2 ? HLF_M2_RST : 1);
   template <int NT>
-  static constexpr int SMEM_DOUBLES = NRAW<NT> * RAWS + 2 * RING + TGT<NT>;
+  static constexpr int TST = MM == 1 ? HLF_M1_TST : (MM == 2 ? HLF_M2_TST : 1);
+  template <int NT>
+  static constexpr int SMEM_DOUBLES = NSRC<NT> * RST<NT> * RAWS + 2 * RING + TST<NT> * TGT<NT>;
 };
 
 struct TParams {
@@ -269,7 +284,10 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   using G = Cfg<MM>;
   constexpr int n1 = G::n1, n = G::n, F = G::F, nh = G::nh, jh = G::jh;
   static_assert(nh == MM + 1, "n/2 == m+1");
-  constexpr int NB = G::template NBUF<NT>;
+  constexpr int RST = G::template RST<NT>;   // raw stages
+  constexpr int TST = G::template TST<NT>;   // target stages
+  constexpr int NSRC = G::template NSRC<NT>;
+  static_assert(RST >= 1 && RST <= 4 && TST >= 1 && TST <= 4, "stage counts");
   constexpr bool MX = NT == 2;                // merged V_x + V_y pressure launch
   constexpr int NTT = G::template NTGT<NT>;   // target fields
   extern __shared__ __align__(128) double smem_raw[];
@@ -281,9 +299,9 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   // raw stages (MX: raw V_x, raw V_y); node index 0 of a row sits at
   // stage base + pre so that TMA row copies start on a 16 B boundary
   double* rawbuf = smem + P.pre;
-  double* ring0 = smem + G::template NRAW<NT> * G::RAWS;
+  double* ring0 = smem + NSRC * RST * G::RAWS;
   double* ring1 = ring0 + G::RING;
-  double* tgs = ring1 + G::RING;              // target stage [t][f][cell], lane-private entries
+  double* tgs = ring1 + G::RING;              // target stages [stage][t][f][cell] (lane-private path: stage 0)
   double* raw = rawbuf;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -327,8 +345,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   const int64_t yo0 = static_cast<int64_t>(ymap(0, my0)) * P.sNx;
   const int64_t yo1 = static_cast<int64_t>(ymap(1, my1)) * P.sNx;
   const bool walls = __syncthreads_or(mx_lane || mx_last || my0 || my1);
-  __shared__ __align__(8) uint64_t rawbar[2];
-  __shared__ __align__(8) uint64_t tgtbar;
+  __shared__ __align__(8) uint64_t rawbar[4];
+  __shared__ __align__(8) uint64_t tgtbar[4];
   uint32_t rphase = 0, tphase = 0;
   // TMA boxes need: no x wrap / mirror inside the row, the two source rows
   // consecutive and unmirrored
@@ -345,7 +363,6 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   // node sx = 32 wraps to 0) still load their rows as TMA boxes (the
   // out-of-range nodes are zero-filled) and patch that one node per row from
   // a register loaded one layer ahead (stored after the box has landed).
-  constexpr int NSRC = MX ? 2 : 1;
   const int psx = P.pre ? 0 : TXC;
   bool mx_psx;
   const int xo_psx = xmap(psx, mx_psx);
@@ -353,16 +370,17 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
 #ifdef HLF_EXP_NORAW
   const bool patch = false;
 #else
-  const bool patch = NB == 1 && !tma_rows && P.tma && !other_mirror && !my0 && !my1 && yo1 == yo0 + P.sNx &&
+  const bool patch = RST == 1 && !tma_rows && P.tma && !other_mirror && !my0 && !my1 && yo1 == yo0 + P.sNx &&
                      (P.pre ? (x0 == 0 && TXC - 1 < P.K[0] && TXC <= P.sNx)
                             : (P.bnd[0] == 0 && x0 + TXC == P.K[0] && x0 + TXC <= P.sNx));
 #endif
   const bool box_rows = tma_rows || patch;
   double pv = 0.0;  // this thread's patch value (row tid % ROWS of source tid / ROWS)
   if (tid == 0) {
-    mbar_init(&rawbar[0], 1);
-    mbar_init(&rawbar[1], 1);
-    mbar_init(&tgtbar, 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&rawbar[i], 1);
+      mbar_init(&tgtbar[i], 1);
+    }
     fence_mbar_init();
     count_path(P.ctr, box_rows, P.tma_t != 0);
   }
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
 #endif
     if (box_rows) {
       // one 4D box (34 nodes x 2 rows x F coefficients x 1 layer) per source
-      const int stage = NB == 2 ? (layer & 1) : 0;
+      const int stage = layer % RST;
       if (patch && tid < NSRC * ROWS) {
         const int si = tid / ROWS, r = tid - si * ROWS;
         const double* base = (si ? P.src2 : P.src) + static_cast<int64_t>(layer) * P.s_layer;
@@ -386,11 +404,11 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       }
       if (tid == 0) {
         constexpr int NS = MX ? 2 : 1;
-        mbar_expect_tx(&rawbar[stage], NS * G::RAW * 8);
+        mbar_expect_tx(&rawbar[stage], NSRC * G::RAW * 8);
         fence_proxy_async();
 #pragma unroll
         for (int si = 0; si < NS; ++si)
-          tma_box(rawbuf + (MX ? si : stage) * G::RAWS - P.pre, &P.tmap[si], x0 - 2 * P.pre, ty - P.pre, layer,
+          tma_box(rawbuf + (stage * NSRC + si) * G::RAWS - P.pre, &P.tmap[si], x0 - 2 * P.pre, ty - P.pre, layer,
                   &rawbar[stage]);
       }
       cp_async_commit();  // empty group: keeps the per-thread group pattern
@@ -398,7 +416,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     }
 #pragma unroll
    for (int si = 0; si < (MX ? 2 : 1); ++si) {
-    double* raw = rawbuf + (MX ? si : (NB == 2 ? (layer & 1) : 0)) * G::RAWS;
+    double* raw = rawbuf + ((layer % RST) * NSRC + si) * G::RAWS;
     const double* base = (si ? P.src2 : P.src) + static_cast<int64_t>(layer) * P.s_layer;
     if constexpr (ROWS % NWARP == 0) {
       // row r = warp + 8 i: coefficient plane (warp >> 1) + 4 i, source row warp & 1
@@ -438,28 +456,29 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       if (neg) raw[e] = -raw[e];
     }
   };
-  auto fix_walls = [&]() {
+  auto fix_walls = [&](int layer) {
+    double* st0 = rawbuf + (layer % RST) * NSRC * G::RAWS;
     if constexpr (MX) {
-      fix_walls_buf(rawbuf, 0);
-      fix_walls_buf(rawbuf + G::RAWS, 1);
+      fix_walls_buf(st0, 0);
+      fix_walls_buf(st0 + G::RAWS, 1);
     } else {
-      fix_walls_buf(raw, P.comp);
+      fix_walls_buf(st0, P.comp);
     }
   };
   auto finish_raw = [&](int layer) {
     cp_async_wait_group1();  // this thread's raw(k+1) landed; its targets(k) may be in flight
     if (box_rows) {
-      const int stage = NB == 2 ? (layer & 1) : 0;
+      const int stage = layer % RST;
       mbar_wait(&rawbar[stage], (rphase >> stage) & 1);
       rphase ^= 1u << stage;
-      if (patch && tid < NSRC * ROWS) {
+      if (patch && tid < NSRC * ROWS) {  // RST == 1
         const int si = tid / ROWS, r = tid - si * ROWS;
-        rawbuf[(MX ? si : stage) * G::RAWS + r * RAWX + psx] = pv;  // after the box: no race with its zero fill
+        rawbuf[(stage * NSRC + si) * G::RAWS + r * RAWX + psx] = pv;  // after the box: no race with its zero fill
       }
     }
     if (walls) {
       __syncthreads();
-      fix_walls();
+      fix_walls(layer);
       if (box_rows) fence_proxy_async();  // generic writes before the next TMA refill of this stage
     }
     __syncthreads();
@@ -528,26 +547,33 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     cp_async_commit();
   };
 
-  // iteration k0-1 is the prologue: it only builds ring layer k0
-  issue_raw(k0);
+  // target boxes of layer kk into stage kk % TST (one per target field)
+  auto issue_tgt = [&](int kk) {
+    const int ts = kk % TST;
+    mbar_expect_tx(&tgtbar[ts], NTT * F * TXC * 8);
+    fence_proxy_async();
+#pragma unroll
+    for (int t = 0; t < NTT; ++t)
+      tma_box(tgs + (ts * NTT + t) * F * TXC, &P.tmapT[t], x0, ty, P.t_zoff + kk, &tgtbar[ts]);
+  };
+  // iteration k0-1 is the prologue: it only builds ring layer k0.  The raw
+  // layers k0 .. k0+RST-1 and the target layers k0 .. k0+TST-2 go out first.
+  for (int l = k0; l < k0 + RST && l <= k1; ++l) issue_raw(l);
   cp_async_commit();  // (empty) targets group of the prologue
+  if (P.tma_t && tid == 0)
+    for (int l = k0; l < k0 + TST - 1 && l < k1; ++l) issue_tgt(l);
   double* ro = ring1;
   double* rn = ring0;
   int emax = 0;  // max |high word| of the written values (finite check)
 #pragma unroll 1
   for (int k = k0 - 1; k < k1; ++k) {
     const bool work = k >= k0;
-    raw = rawbuf + (NB == 2 ? ((k + 1) & 1) : 0) * G::RAWS;
+    raw = rawbuf + ((k + 1) % RST) * NSRC * G::RAWS;
     finish_raw(k + 1);  // raw(k+1) landed; every warp left the previous Z + CK stage
-    if (P.tma_t && work && tid == 0) {
-      // targets of layer k, one box per target field; consumed after the Z + CK sums
-      mbar_expect_tx(&tgtbar, NTT * F * TXC * 8);
-      fence_proxy_async();
-#pragma unroll
-      for (int t = 0; t < NTT; ++t) tma_box(tgs + t * F * TXC, &P.tmapT[t], x0, ty, P.t_zoff + k, &tgtbar);
-    }
-    if (NB == 2) {
-      if (k + 1 < k1) issue_raw(k + 2); else cp_async_commit();
+    if (P.tma_t && work && tid == 0 && k + TST - 1 < k1) {
+      // targets of layer k + TST - 1 into the stage layer k - 1 used (its
+      // epilogue is over: every warp passed the barrier in finish_raw)
+      issue_tgt(k + TST - 1);
     }
 #ifndef HLF_EXP_NOXY
     if (MX && warp >= 2 * n1) {
@@ -555,7 +581,7 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     } else if constexpr (MX) {
       const int lz = warp >> 1;
       double* wb = rn + lz * TXC + lane;
-      const double* rbx = rawbuf + lz * 2 * RAWX + lane;
+      const double* rbx = raw + lz * 2 * RAWX + lane;
       const double* rby = rbx + G::RAWS;
 #ifndef HLF_XY_RMW
       xy_merged<MM>(warp & 1, P, rbx, rby, wb);
@@ -573,9 +599,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     }
 #endif
     __syncthreads();
-    if (NB == 1) {
-      if (k + 1 < k1) issue_raw(k + 2); else cp_async_commit();
-    }
+    // the stage of raw(k+1) is free again: refill it with raw(k+1+RST)
+    if (k + 1 + RST <= k1) issue_raw(k + 1 + RST); else cp_async_commit();
 
 #ifdef HLF_EXP_NOZCK
     if (0) {
@@ -588,8 +613,9 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       else if constexpr (!V7) z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
       const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
       if (P.tma_t) {
-        mbar_wait(&tgtbar, tphase);
-        tphase ^= 1u;
+        const int ts = k % TST;
+        mbar_wait(&tgtbar[ts], (tphase >> ts) & 1);
+        tphase ^= 1u << ts;
       } else {
         cp_async_wait_group1();  // this lane's targets(k) landed; raw(k+2) may be in flight
       }
@@ -609,7 +635,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
         const int f0 = (sx * n1 + sy) * n1 + sz;
         double* dp = P.dst[t] + obase + f0 * P.t_plane32;
         asm("" : "+l"(dp));  // keep dp a base register: one IMAD.WIDE per output address
-        const double* tp = tgs + (t * F + f0) * TXC + zcell;
+        // TMA targets sit in stage k % TST; the lane-private cp.async path uses stage 0
+        const double* tp = tgs + ((P.tma_t ? k % TST : 0) * NTT + t) * F * TXC + f0 * TXC + zcell;
 #ifndef HLF_EXP_NOCK
         if constexpr (V7S) v7_zck(c, PX, PY, PZ, P, ro + cbase, rn + cbase, cz, zg, acc);
         else if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);

@@ -1,0 +1,465 @@
+// 3D Hermite-leapfrog half steps with a spatially varying coefficient
+// ap = -(c0 + c1 prod_ax sin(w_ax x_ax + phase_ax))  (ap = -c^2, c^2 separable),
+// av a scalar, m = 1..3: the variable-coefficient CK recurrence of
+// ck_recurrence_variable (stepper1d.cpp:22-38) generalised to d = 3 with
+// truncated tensor products (tensor_multiply, jet.cpp:109-121).
+//
+// The ap jets are generated on the fly at every target node (no stored
+// coefficient grids: the traffic stays the 24 B per DOF-update of the
+// constant-coefficient kernels), and because the jet is
+// e0 (-c0) plus an outer product (-c1 s_x (x) s_y (x) s_z), the truncated
+// product ap (.) X is -c0 X - c1 S_x S_y S_z X with S_a the 1D truncated
+// Cauchy product along axis a: 3 n^2 lines x n(n+1)/2 multiply-adds instead
+// of the (n(n+1)/2)^3 of a general n^3 jet.
+//
+// One warp per target node, the node's n^3 tensors in padded shared memory
+// (strides n+1 and n(n+1)+1 so that lines along every axis are bank
+// friendly), lanes over lines (sweeps, products) or entries (derivatives).
+// Per node, with P_r / V_r the CK tables (seed zero for the target's family):
+//   pressure:  D = sum_c d_c recon(V_c);  P_1 = ap (.) D;  P_{r+2} = ap (.) (av Lap P_r)
+//              p += sum_{r odd} w_r P_r           (advance_p, stepper1d.cpp:147-156)
+//   velocity:  P_0 = recon(p);  V_c[r] = av d_c P_{r-1};  P_{r+1} = ap (.) (av Lap P_{r-1})
+//              v_c += sum_{r odd} w_r V_c[r]      (advance_v, stepper1d.cpp:158-166)
+// with d_c the truncated scaled derivative (jet_differentiate, jet.cpp:20-31)
+// and Lap = sum_c d_c d_c (the two derivatives of the recurrence; av is a
+// scalar).  Arithmetic is reordered against the oracle (FMA, separable
+// products), so parity is at the 1e-12 bar, not bit-identical.
+#include "hlf_internal.cuh"
+
+namespace hlfk {
+namespace {
+
+constexpr int WARPS = 4;
+
+template <int MM>
+struct V3 {
+  static constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1 * n1, E = n * n * n;
+  static constexpr int SZ = 1, SY = n + 1, SX = n * (n + 1) + 1;  // padded strides (odd)
+  static constexpr int T = n * SX;                                 // doubles per padded tensor
+  static constexpr int NBUF = 3;
+  static constexpr int SMEM = WARPS * NBUF * T;                    // doubles per CTA
+};
+
+template <int MM>
+__device__ __forceinline__ int pidx(int qx, int qy, int qz) {
+  return qx * V3<MM>::SX + qy * V3<MM>::SY + qz;
+}
+
+// line l (0 .. n^2-1) along axis ax: base offset and stride in the padded layout
+template <int MM>
+__device__ __forceinline__ void line_of(int ax, int l, int& base, int& stride) {
+  constexpr int n = V3<MM>::n;
+  const int a = l / n, b = l - (l / n) * n;
+  if (ax == 0) {
+    base = pidx<MM>(0, a, b);
+    stride = V3<MM>::SX;
+  } else if (ax == 1) {
+    base = pidx<MM>(a, 0, b);
+    stride = V3<MM>::SY;
+  } else {
+    base = pidx<MM>(a, b, 0);
+    stride = 1;
+  }
+}
+
+// scaled jet of sin(w x + ph) at x, spacing h: s[k] = (w h)^k / k! sin(w x + ph + k pi/2) (sin_jet, jet.cpp)
+template <int N>
+__device__ __forceinline__ void sin_jet_dev(double w, double ph, double x, double h, double (&s)[N]) {
+  double sn, cs;
+  sincos(w * x + ph, &sn, &cs);
+  double f = 1.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int r = k & 3;
+    s[k] = f * (r == 0 ? sn : (r == 1 ? cs : (r == 2 ? -sn : -cs)));
+    f = f * (w * h) / (k + 1);
+  }
+}
+
+struct V3Params {
+  HalfParams hp;
+  double c0, c1, w[3], ph[3];
+  double x0[3];  // coordinate of target node 0 per axis
+};
+
+template <int MM, int KIND>
+__global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Params Q) {
+  using C = V3<MM>;
+  constexpr int n1 = C::n1, n = C::n, F = C::F, E = C::E, T = C::T;
+  constexpr int NOUT = KIND == VEL ? 3 : 1;
+  constexpr int NSRC = KIND == VEL ? 1 : 3;
+  constexpr int FL = (F + 31) / 32;  // output entries per lane
+  const HalfParams& P = Q.hp;
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* A = sm + warp * C::NBUF * T;
+  double* B = A + T;
+  double* Cb = B + T;
+  const double inv_h = 1.0 / P.h;
+
+  const int64_t total = static_cast<int64_t>(P.tNx) * P.tNy * P.tNz;
+  const int64_t stride_nodes = static_cast<int64_t>(gridDim.x) * WARPS;
+#pragma unroll 1
+  for (int64_t node = static_cast<int64_t>(blockIdx.x) * WARPS + warp; node < total; node += stride_nodes) {
+    int t[3];
+    t[0] = static_cast<int>(node % P.tNx);
+    const int64_t rest = node / P.tNx;
+    t[1] = static_cast<int>(rest % P.tNy);
+    t[2] = static_cast<int>(rest / P.tNy);
+    const int64_t toff = static_cast<int64_t>(P.t_zoff + t[2]) * P.t_layer + static_cast<int64_t>(t[1]) * P.tNx + t[0];
+
+    // corner addresses and wall flips (as half_generic)
+    int64_t coff[8];
+    int cflip[8];
+#pragma unroll
+    for (int corner = 0; corner < 8; ++corner) {
+      int s[3];
+      int flip = 0;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const int side = (corner >> ax) & 1;
+        int q = KIND == VEL ? t[ax] + side : t[ax] - 1 + side;
+        if (ax < 2) {
+          if (P.bnd[ax] == 0) {
+            if (q >= P.K[ax]) q -= P.K[ax];
+            if (q < 0) q += P.K[ax];
+          } else if (KIND == PRE) {
+            if (q < 0) {
+              q = 0;
+              flip |= 1 << ax;
+            } else if (q >= P.K[ax]) {
+              q = P.K[ax] - 1;
+              flip |= 1 << ax;
+            }
+          }
+        }
+        s[ax] = q;
+      }
+      coff[corner] = static_cast<int64_t>(P.s_zoff + s[2]) * P.s_layer + static_cast<int64_t>(s[1]) * P.sNx + s[0];
+      cflip[corner] = flip;
+    }
+
+    // this node's separable ap: per-axis sin jets
+    double sx[n], sy[n], sz[n];
+    sin_jet_dev<n>(Q.w[0], Q.ph[0], Q.x0[0] + t[0] * P.h, P.h, sx);
+    sin_jet_dev<n>(Q.w[1], Q.ph[1], Q.x0[1] + t[1] * P.h, P.h, sy);
+    sin_jet_dev<n>(Q.w[2], Q.ph[2], Q.x0[2] + t[2] * P.h, P.h, sz);
+
+    // targets of this lane's output entries
+    double tgt[NOUT][FL];
+#pragma unroll
+    for (int c = 0; c < NOUT; ++c)
+#pragma unroll
+      for (int j = 0; j < FL; ++j) {
+        const int f = lane + 32 * j;
+        tgt[c][j] = f < F ? P.dst[c][toff + static_cast<int64_t>(f) * P.t_coef] : 0.0;
+      }
+
+    // ---- reconstruction of one source field into Cb (x, y, z sweeps of M)
+    auto reconstruct = [&](int comp) {
+      const double* src = P.src[comp];
+      for (int e = lane; e < E; e += 32) {
+        const int qx = e / (n * n), qy = (e / n) % n, qz = e % n;
+        const int q[3] = {qx, qy, qz};
+        int corner = 0, f = 0;
+        double sign = 1.0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          const int side = q[ax] / n1, l = q[ax] - side * n1;
+          corner |= side << ax;
+          f = f * n1 + l;
+        }
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          if ((cflip[corner] >> ax) & 1) {
+            const int l = q[ax] % n1;
+            if (l & 1) sign = -sign;
+            if (comp != ax) sign = -sign;  // tangential velocity is odd across the wall
+          }
+        }
+        A[pidx<MM>(qx, qy, qz)] = sign * __ldg(src + coff[corner] + static_cast<int64_t>(f) * P.s_coef);
+      }
+      __syncwarp();
+      double* in = A;
+      double* out = Cb;
+#pragma unroll 1
+      for (int ax = 0; ax < 3; ++ax) {
+        for (int l = lane; l < n * n; l += 32) {
+          int base, st;
+          line_of<MM>(ax, l, base, st);
+          double v[n];
+#pragma unroll
+          for (int s = 0; s < n; ++s) v[s] = in[base + s * st];
+#pragma unroll
+          for (int r = 0; r < n; ++r) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s = 0; s < n; ++s) acc = fma(P.M[r * n + s], v[s], acc);
+            out[base + r * st] = acc;
+          }
+        }
+        __syncwarp();
+        double* tmp = in;
+        in = out;
+        out = tmp;
+      }
+      // after three sweeps the result is in A (in) -- copy pointer semantics:
+      // sweeps A->Cb, Cb->A, A->Cb: the result sits in Cb
+    };
+
+    // X <- ap (.) X in place: X = -c0 X - c1 S_x S_y S_z X, with the S passes through B
+    auto ap_times = [&](double* X) {
+      // B <- X
+      for (int e = lane; e < E; e += 32) {
+        const int qx = e / (n * n), qy = (e / n) % n, qz = e % n;
+        B[pidx<MM>(qx, qy, qz)] = X[pidx<MM>(qx, qy, qz)];
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int ax = 2; ax >= 0; --ax) {
+        const double* s = ax == 0 ? sx : (ax == 1 ? sy : sz);
+        for (int l = lane; l < n * n; l += 32) {
+          int base, st;
+          line_of<MM>(ax, l, base, st);
+          double v[n];
+#pragma unroll
+          for (int i = 0; i < n; ++i) v[i] = B[base + i * st];
+#pragma unroll
+          for (int i = n - 1; i >= 0; --i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j <= i; ++j) acc = fma(s[j], v[i - j], acc);
+            B[base + i * st] = acc;
+          }
+        }
+        __syncwarp();
+      }
+      for (int e = lane; e < E; e += 32) {
+        const int qx = e / (n * n), qy = (e / n) % n, qz = e % n;
+        const int k = pidx<MM>(qx, qy, qz);
+        X[k] = fma(-Q.c1, B[k], -Q.c0 * X[k]);
+      }
+      __syncwarp();
+    };
+
+    // Y <- av Lap X (truncated second derivatives, jet_differentiate twice per axis)
+    auto av_lap = [&](const double* X, double* Y) {
+      for (int e = lane; e < E; e += 32) {
+        const int q[3] = {e / (n * n), (e / n) % n, e % n};
+        double acc = 0.0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          if (q[ax] + 2 < n) {
+            int r[3] = {q[0], q[1], q[2]};
+            r[ax] += 2;
+            acc = fma(static_cast<double>((q[ax] + 1) * (q[ax] + 2)) * inv_h * inv_h, X[pidx<MM>(r[0], r[1], r[2])], acc);
+          }
+        }
+        Y[pidx<MM>(q[0], q[1], q[2])] = P.av * acc;
+      }
+      __syncwarp();
+    };
+
+    if constexpr (KIND == PRE) {
+      // D = sum_c d_c recon(V_c), accumulated in B... B is the product scratch,
+      // so D goes to A after the reconstructions (kept in registers meanwhile)
+      double dsum[(E + 31) / 32];
+#pragma unroll
+      for (int j = 0; j < (E + 31) / 32; ++j) dsum[j] = 0.0;
+#pragma unroll 1
+      for (int comp = 0; comp < NSRC; ++comp) {
+        reconstruct(comp);  // -> Cb
+#pragma unroll
+        for (int j = 0; j < (E + 31) / 32; ++j) {
+          const int e = lane + 32 * j;
+          if (e < E) {
+            const int q[3] = {e / (n * n), (e / n) % n, e % n};
+            if (q[comp] + 1 < n) {
+              int r[3] = {q[0], q[1], q[2]};
+              r[comp] += 1;
+              dsum[j] = fma(static_cast<double>(q[comp] + 1) * inv_h, Cb[pidx<MM>(r[0], r[1], r[2])], dsum[j]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      // P_1 = ap (.) D, in A
+#pragma unroll
+      for (int j = 0; j < (E + 31) / 32; ++j) {
+        const int e = lane + 32 * j;
+        if (e < E) A[pidx<MM>(e / (n * n), (e / n) % n, e % n)] = dsum[j];
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int r = 1; r < n; r += 2) {
+        if (r > 1) {
+          av_lap(A, Cb);  // Cb = av Lap P_{r-2}
+          double* tmp = A;
+          A = Cb;
+          Cb = tmp;
+        }
+        ap_times(A);      // A = P_r
+        const double w = P.w[r];
+#pragma unroll
+        for (int j = 0; j < FL; ++j) {
+          const int f = lane + 32 * j;
+          if (f < F) {
+            const int o[3] = {f / (n1 * n1), (f / n1) % n1, f % n1};
+            tgt[0][j] = fma(w, A[pidx<MM>(o[0], o[1], o[2])], tgt[0][j]);
+          }
+        }
+      }
+    } else {
+      reconstruct(0);  // P_0 in Cb
+      double* Pc = Cb;
+      double* Xs = A;
+#pragma unroll 1
+      for (int r = 1; r < n; r += 2) {
+        // V_c[r] = av d_c P_{r-1}: this lane's output entries
+        const double w = P.w[r];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int j = 0; j < FL; ++j) {
+            const int f = lane + 32 * j;
+            if (f < F) {
+              int o[3] = {f / (n1 * n1), (f / n1) % n1, f % n1};
+              const int qc = o[c];
+              o[c] += 1;
+              const double dv = static_cast<double>(qc + 1) * inv_h * Pc[pidx<MM>(o[0], o[1], o[2])];
+              tgt[c][j] = fma(w, P.av * dv, tgt[c][j]);  // qc + 1 <= m + 1 < n: never truncated here
+            }
+          }
+        if (r + 2 < n) {
+          av_lap(Pc, Xs);   // Xs = av Lap P_{r-1}
+          ap_times(Xs);     // Xs = P_{r+1}
+          double* tmp = Pc;
+          Pc = Xs;
+          Xs = tmp;
+        }
+      }
+      // keep A/B/Cb roles consistent for the next node
+      (void)Xs;
+    }
+
+    // store + finite flag
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < NOUT; ++c)
+#pragma unroll
+      for (int j = 0; j < FL; ++j) {
+        const int f = lane + 32 * j;
+        if (f < F) {
+          bad |= !isfinite(tgt[c][j]);
+          P.dst[c][toff + static_cast<int64_t>(f) * P.t_coef] = tgt[c][j];
+        }
+      }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && P.step >= 0) report_nonfinite(P.flag, P.step);
+    // restore the buffer roles (the pressure loop may have swapped them)
+    A = sm + warp * C::NBUF * T;
+    B = A + T;
+    Cb = B + T;
+    __syncwarp();
+  }
+}
+
+template <int MM>
+int launch_m(HalfKind kind, const V3Params& q, cudaStream_t st) {
+  const size_t smem = sizeof(double) * V3<MM>::SMEM;
+  static std::atomic<unsigned long long> cfg_pre{0}, cfg_vel{0};
+  const int64_t total = static_cast<int64_t>(q.hp.tNx) * q.hp.tNy * q.hp.tNz;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (total + WARPS - 1) / WARPS;
+  const unsigned blocks = static_cast<unsigned>(want < 64LL * sms ? want : 64LL * sms);
+  if (kind == VEL) {
+    ensure_smem_opt_in(var3d<MM, VEL>, static_cast<int>(smem), cfg_vel);
+    var3d<MM, VEL><<<blocks, WARPS * 32, smem, st>>>(q);
+  } else {
+    ensure_smem_opt_in(var3d<MM, PRE>, static_cast<int>(smem), cfg_pre);
+    var3d<MM, PRE><<<blocks, WARPS * 32, smem, st>>>(q);
+  }
+  mark_launch(q.hp, st);
+  return 1;
+}
+
+// separable coefficient jets on the nodes of one grid, stored like hlf_set_coeff's
+// ([z][E][y][x]): jet = -(c0 e_0 + c1 s_x (x) s_y (x) s_z)
+template <int D>
+__global__ void fill_sep_coeff(double* dst, int Nx, int Ny, int Nz, int n, double h, double x0, double y0, double z0,
+                               double c0, double c1, double wx, double wy, double wz, double px, double py,
+                               double pz) {
+  const int64_t total = static_cast<int64_t>(Nx) * Ny * Nz;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int ix = static_cast<int>(i % Nx);
+  const int iy = static_cast<int>((i / Nx) % Ny);
+  const int iz = static_cast<int>(i / (static_cast<int64_t>(Nx) * Ny));
+  double s[3][kMaxN];
+  const double w[3] = {wx, wy, wz}, ph[3] = {px, py, pz}, xx[3] = {x0 + ix * h, y0 + iy * h, z0 + iz * h};
+  for (int ax = 0; ax < D; ++ax) {
+    double sn, cs;
+    sincos(w[ax] * xx[ax] + ph[ax], &sn, &cs);
+    double f = 1.0;
+    for (int k = 0; k < n; ++k) {
+      const int r = k & 3;
+      s[ax][k] = f * (r == 0 ? sn : (r == 1 ? cs : (r == 2 ? -sn : -cs)));
+      f = f * (w[ax] * h) / (k + 1);
+    }
+  }
+  const int64_t plane = static_cast<int64_t>(Nx) * Ny;
+  const int E = D == 1 ? n : (D == 2 ? n * n : n * n * n);
+  for (int e = 0; e < E; ++e) {
+    int q[3] = {0, 0, 0}, r = e;
+    for (int ax = D - 1; ax >= 0; --ax) {
+      q[ax] = r % n;
+      r /= n;
+    }
+    double prod = c1;
+    for (int ax = 0; ax < D; ++ax) prod *= s[ax][q[ax]];
+    const double v = -(prod + (e == 0 ? c0 : 0.0));
+    dst[(static_cast<int64_t>(iz) * E + e) * plane + static_cast<int64_t>(iy) * Nx + ix] = v;
+  }
+}
+
+}  // namespace
+
+bool var3d_supported(int m) { return m >= 1 && m <= 3; }
+
+int launch_half_var3d(int m, HalfKind kind, const HalfParams& p, const double* sep, const double* x0,
+                      cudaStream_t st) {
+  V3Params q;
+  q.hp = p;
+  q.c0 = sep[0];
+  q.c1 = sep[1];
+  for (int a = 0; a < 3; ++a) {
+    q.w[a] = sep[2 + a];
+    q.ph[a] = sep[5 + a];
+    q.x0[a] = x0[a];
+  }
+  switch (m) {
+    case 1: return launch_m<1>(kind, q, st);
+    case 2: return launch_m<2>(kind, q, st);
+    case 3: return launch_m<3>(kind, q, st);
+    default: return -1;
+  }
+}
+
+int launch_fill_sep_coeff(double* dst, int d, const int* N, int n, double h, const double* x0, const double* sep,
+                          cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(N[0]) * N[1] * N[2];
+  const unsigned blocks = static_cast<unsigned>((total + 127) / 128);
+  if (d == 1)
+    fill_sep_coeff<1><<<blocks, 128, 0, st>>>(dst, N[0], N[1], N[2], n, h, x0[0], x0[1], x0[2], sep[0], sep[1],
+                                              sep[2], sep[3], sep[4], sep[5], sep[6], sep[7]);
+  else if (d == 2)
+    fill_sep_coeff<2><<<blocks, 128, 0, st>>>(dst, N[0], N[1], N[2], n, h, x0[0], x0[1], x0[2], sep[0], sep[1],
+                                              sep[2], sep[3], sep[4], sep[5], sep[6], sep[7]);
+  else
+    fill_sep_coeff<3><<<blocks, 128, 0, st>>>(dst, N[0], N[1], N[2], n, h, x0[0], x0[1], x0[2], sep[0], sep[1],
+                                              sep[2], sep[3], sep[4], sep[5], sep[6], sep[7]);
+  return 1;
+}
+
+}  // namespace hlfk

@@ -291,6 +291,13 @@ class Stepper:
             raise ValueError("coefficient buffer has the wrong size")
         self._c(self._L.hlf_set_coeff(self._h, grid, a.ctypes.data))
 
+    def set_coeff_separable(self, c0: float, c1: float, w: Sequence[float], phase: Sequence[float]):
+        """ap = -(c0 + c1 prod sin(w x + phase)) on both grids
+        (hlf_set_coeff_separable; generated in-kernel in 3D for m <= 3)."""
+        w3 = (C.c_double * 3)(*(list(w) + [0.0] * (3 - len(w))))
+        p3 = (C.c_double * 3)(*(list(phase) + [0.0] * (3 - len(phase))))
+        self._c(self._L.hlf_set_coeff_separable(self._h, c0, c1, w3, p3))
+
     def set_forcing(self, grid: int, table: np.ndarray):
         """1D forcing jets z_r (r = 0..2m, each 2m+2 long) at every node of
         `grid` for the next half step updating that grid (hlf_set_forcing:
