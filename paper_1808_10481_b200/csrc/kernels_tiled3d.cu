@@ -69,10 +69,10 @@ struct Cfg {
   // are deep; at m = 3 there is no room for a second stage (and an iteration
   // covers the latency).  HLF_M1_RST / _TST, HLF_M2_RST / _TST override.
 #ifndef HLF_M1_RST
-#define HLF_M1_RST 4
+#define HLF_M1_RST 2
 #endif
 #ifndef HLF_M1_TST
-#define HLF_M1_TST 3
+#define HLF_M1_TST 2
 #endif
 #ifndef HLF_M2_RST
 #define HLF_M2_RST 1

@@ -108,17 +108,16 @@ __global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Pa
     t[2] = static_cast<int>(rest / P.tNy);
     const int64_t toff = static_cast<int64_t>(P.t_zoff + t[2]) * P.t_layer + static_cast<int64_t>(t[1]) * P.tNx + t[0];
 
-    // corner addresses and wall flips (as half_generic)
-    int64_t coff[8];
-    int cflip[8];
+    // per axis and side: the source node's offset and whether it is a wall
+    // mirror (as half_generic's corner maps); a corner's address is the sum
+    int64_t aoff[3][2];
+    bool aflip[3][2];
 #pragma unroll
-    for (int corner = 0; corner < 8; ++corner) {
-      int s[3];
-      int flip = 0;
+    for (int ax = 0; ax < 3; ++ax)
 #pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        const int side = (corner >> ax) & 1;
+      for (int side = 0; side < 2; ++side) {
         int q = KIND == VEL ? t[ax] + side : t[ax] - 1 + side;
+        bool flip = false;
         if (ax < 2) {
           if (P.bnd[ax] == 0) {
             if (q >= P.K[ax]) q -= P.K[ax];
@@ -126,18 +125,17 @@ __global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Pa
           } else if (KIND == PRE) {
             if (q < 0) {
               q = 0;
-              flip |= 1 << ax;
+              flip = true;
             } else if (q >= P.K[ax]) {
               q = P.K[ax] - 1;
-              flip |= 1 << ax;
+              flip = true;
             }
           }
         }
-        s[ax] = q;
+        aflip[ax][side] = flip;
+        aoff[ax][side] = ax == 0 ? q : (ax == 1 ? static_cast<int64_t>(q) * P.sNx
+                                                : static_cast<int64_t>(P.s_zoff + q) * P.s_layer);
       }
-      coff[corner] = static_cast<int64_t>(P.s_zoff + s[2]) * P.s_layer + static_cast<int64_t>(s[1]) * P.sNx + s[0];
-      cflip[corner] = flip;
-    }
 
     // this node's separable ap: per-axis sin jets
     double sx[n], sy[n], sz[n];
@@ -158,26 +156,24 @@ __global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Pa
     // ---- reconstruction of one source field into Cb (x, y, z sweeps of M)
     auto reconstruct = [&](int comp) {
       const double* src = P.src[comp];
+#pragma unroll 4
       for (int e = lane; e < E; e += 32) {
         const int qx = e / (n * n), qy = (e / n) % n, qz = e % n;
         const int q[3] = {qx, qy, qz};
-        int corner = 0, f = 0;
+        int f = 0;
+        int64_t off = 0;
         double sign = 1.0;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
-          const int side = q[ax] / n1, l = q[ax] - side * n1;
-          corner |= side << ax;
+          const int side = q[ax] >= n1, l = q[ax] - side * n1;
           f = f * n1 + l;
-        }
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-          if ((cflip[corner] >> ax) & 1) {
-            const int l = q[ax] % n1;
+          off += side ? aoff[ax][1] : aoff[ax][0];
+          if (side ? aflip[ax][1] : aflip[ax][0]) {
             if (l & 1) sign = -sign;
             if (comp != ax) sign = -sign;  // tangential velocity is odd across the wall
           }
         }
-        A[pidx<MM>(qx, qy, qz)] = sign * __ldg(src + coff[corner] + static_cast<int64_t>(f) * P.s_coef);
+        A[pidx<MM>(qx, qy, qz)] = sign * __ldg(src + off + static_cast<int64_t>(f) * P.s_coef);
       }
       __syncwarp();
       double* in = A;
@@ -215,9 +211,9 @@ __global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Pa
         B[pidx<MM>(qx, qy, qz)] = X[pidx<MM>(qx, qy, qz)];
       }
       __syncwarp();
-#pragma unroll 1
+#pragma unroll
       for (int ax = 2; ax >= 0; --ax) {
-        const double* s = ax == 0 ? sx : (ax == 1 ? sy : sz);
+        const double* s = ax == 0 ? sx : (ax == 1 ? sy : sz);  // compile-time after unrolling
         for (int l = lane; l < n * n; l += 32) {
           int base, st;
           line_of<MM>(ax, l, base, st);

@@ -12,7 +12,10 @@ K = Ks[0]
 steps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 variant = int(sys.argv[5]) if len(sys.argv) > 5 else -1
 stream = torch.cuda.Stream()
-g = H.Stepper(H.Grid([-1.0] * d, 2.0 / K, tuple(Ks)), m, stream=stream.cuda_stream)
+var = os.environ.get("HLF_VAR_SEP") is not None  # variable c^2 = 1 + prod sin / 2 (var2d / var3d)
+g = H.Stepper(H.Grid([-1.0] * d, 2.0 / K, tuple(Ks)), m, stream=stream.cuda_stream, variable_ap=var)
+if var:
+    g.set_coeff_separable(1.0, 0.5, [math.pi] * d, [0.0] * d)
 if variant >= 0:
     g.kernel_variant = variant
 pi = math.pi
