@@ -259,7 +259,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--configs", action="store_true",
+                    help="instead of the headline line: one JSON line (with clocks) per SURVEY.md sec. 8(d) "
+                         "configuration, tools/bench_configs.py")
     args = ap.parse_args()
+    if args.configs:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_configs
+        sys.argv = [sys.argv[0]]
+        bench_configs.main()
+        return
     if args.impl == "reference":
         run_reference_impl(args)
         return
