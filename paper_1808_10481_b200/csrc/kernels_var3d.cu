@@ -34,7 +34,12 @@ constexpr int WARPS = 4;
 template <int MM>
 struct V3 {
   static constexpr int n1 = MM + 1, n = 2 * MM + 2, F = n1 * n1 * n1, E = n * n * n;
-  static constexpr int SZ = 1, SY = n + 1, SX = n * (n + 1) + 1;  // padded strides (odd)
+  // strides chosen by a bank-conflict search over the access patterns (lines
+  // along each axis with lanes over the other two, entries with lanes over
+  // z then y): 2, 4 and 2 wavefronts per 32-lane LDS.64 for x-, y- and z-lines
+  // and 2 for entries at n = 8 (the first layout, SY = n+1 and SX = n(n+1)+1,
+  // was 4 everywhere: ncu showed 50 % of the shared wavefronts as conflicts)
+  static constexpr int SZ = 1, SY = n, SX = n * n + 1;
   static constexpr int T = n * SX;                                 // doubles per padded tensor
   static constexpr int NBUF = 3;
   static constexpr int SMEM = WARPS * NBUF * T;                    // doubles per CTA
@@ -57,7 +62,7 @@ __device__ __forceinline__ void line_of(int ax, int l, int& base, int& stride) {
     base = pidx<MM>(a, 0, b);
     stride = V3<MM>::SY;
   } else {
-    base = pidx<MM>(a, b, 0);
+    base = pidx<MM>(b, a, 0);  // lanes run along x here (conflict-free with SX = n^2 + 1)
     stride = 1;
   }
 }
@@ -205,37 +210,28 @@ __global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Pa
 
     // X <- ap (.) X in place: X = -c0 X - c1 S_x S_y S_z X, with the S passes through B
     auto ap_times = [&](double* X) {
-      // B <- X
-      for (int e = lane; e < E; e += 32) {
-        const int qx = e / (n * n), qy = (e / n) % n, qz = e % n;
-        B[pidx<MM>(qx, qy, qz)] = X[pidx<MM>(qx, qy, qz)];
-      }
-      __syncwarp();
+      // z pass X -> B, y pass in B, x pass B -> X fused with -c0 X - c1 (.)
 #pragma unroll
       for (int ax = 2; ax >= 0; --ax) {
         const double* s = ax == 0 ? sx : (ax == 1 ? sy : sz);  // compile-time after unrolling
+        const double* in = ax == 2 ? X : B;
         for (int l = lane; l < n * n; l += 32) {
           int base, st;
           line_of<MM>(ax, l, base, st);
           double v[n];
 #pragma unroll
-          for (int i = 0; i < n; ++i) v[i] = B[base + i * st];
+          for (int i = 0; i < n; ++i) v[i] = in[base + i * st];
 #pragma unroll
           for (int i = n - 1; i >= 0; --i) {
             double acc = 0.0;
 #pragma unroll
             for (int j = 0; j <= i; ++j) acc = fma(s[j], v[i - j], acc);
-            B[base + i * st] = acc;
+            if (ax == 0) X[base + i * st] = fma(-Q.c1, acc, -Q.c0 * X[base + i * st]);
+            else B[base + i * st] = acc;
           }
         }
         __syncwarp();
       }
-      for (int e = lane; e < E; e += 32) {
-        const int qx = e / (n * n), qy = (e / n) % n, qz = e % n;
-        const int k = pidx<MM>(qx, qy, qz);
-        X[k] = fma(-Q.c1, B[k], -Q.c0 * X[k]);
-      }
-      __syncwarp();
     };
 
     // Y <- av Lap X (truncated second derivatives, jet_differentiate twice per axis)
