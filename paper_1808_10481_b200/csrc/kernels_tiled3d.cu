@@ -43,7 +43,13 @@ constexpr int TXC = 32;         // cells per CTA row (= lanes)
 constexpr int RAWX = TXC + 2;   // source row stride: 33 nodes used, 34 = 17 x 16 B (TMA row copies)
 constexpr int NWARP = 8;
 constexpr int NTHREADS = NWARP * 32;
-constexpr int ZC = 64;          // target layers per CTA (with TMA loads: 64 +0.9 % over 128, 256 -1.5 %)
+#ifndef HLF_ZC
+#define HLF_ZC 64
+#endif
+#ifndef HLF_ZSEL_SELECT
+#define HLF_ZSEL_SELECT 0  // 1: the V_z launch shifts with per-column selects instead of shifted M rows
+#endif
+constexpr int ZC = HLF_ZC;      // target layers per CTA (with TMA loads: 64 +0.9 % over 128, 256 -1.5 %)
 constexpr int kMaxB = 20;       // multi-indices |b| <= 3
 
 template <int MM>
@@ -208,7 +214,11 @@ __device__ __forceinline__ void v7_zck(int c, int PX, int PY, int PZ, const TPar
   } else if (c == 1) {
     if (PY) v7_m3_zck_c1_s0(P, ro, rn, cz, g, PZ, acc); else v7_m3_zck_c1_s1(P, ro, rn, cz, g, PZ, acc);
   } else {
+#if HLF_ZSEL_SELECT
     v7_m3_zck_zsel(P, ro, rn, cz, g, PZ, acc);
+#else
+    v7_m3_zck_c0_s0(P, ro, rn, cz, g, PZ, acc);  // the z shift is in the PZ = 0 lanes' rows (cz)
+#endif
   }
 }
 
@@ -511,11 +521,19 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
   const bool zactive = x0 + zcell < P.tNx;
   double cz[nh][n1];
   const double zg = PZ ? -1.0 : 1.0;
+  // V_z pressure launch (streaming): the PZ = 0 lanes read P~ one z index up
+  // (the divergence term's shift); rows 2 iz + 2 have the class's own row
+  // parity, so their z lines use the same sum / difference pattern and the
+  // shift is just the next row of M (row 2m + 2 does not exist: zero)
+  const bool zshift = V7S && NT == 1 && P.comp == 2 && PZ == 0 && !HLF_ZSEL_SELECT;
   if constexpr (V7) {
 #pragma unroll
     for (int iz = 0; iz < nh; ++iz)
 #pragma unroll
-      for (int l = 0; l < n1; ++l) cz[iz][l] = P.ML[(PZ + 2 * iz) * n1 + l];
+      for (int l = 0; l < n1; ++l) {
+        const int row = PZ + 2 * iz + (zshift ? 2 : 0);
+        cz[iz][l] = row < n ? P.ML[(row < n ? row : 0) * n1 + l] : 0.0;
+      }
   }
 
   // Targets of layer kk for this lane's own outputs (the entries its epilogue
@@ -619,7 +637,9 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
       } else {
         cp_async_wait_group1();  // this lane's targets(k) landed; raw(k+2) may be in flight
       }
-#pragma unroll 1
+      // the velocity launch's three components unrolled (their CK chains
+      // interleave: 66.2 -> 63.4 ms at 512x512x256)
+#pragma unroll
       for (int t = 0; t < NTT; ++t) {
         const int c = MX ? -1 : (NT == 3 ? t : P.comp);  // -1: shifts already in the XY rows
         double acc[jh][jh][jh];
