@@ -46,6 +46,9 @@ constexpr int NTHREADS = NWARP * 32;
 #ifndef HLF_ZC
 #define HLF_ZC 64
 #endif
+#ifndef HLF_L2HINT
+#define HLF_L2HINT 1  // evict-first L2 policy for the target loads and stores (velocity, V_z launches)
+#endif
 #ifndef HLF_ZSEL_SELECT
 #define HLF_ZSEL_SELECT 0  // 1: the V_z launch shifts with per-column selects instead of shifted M rows
 #endif
@@ -136,6 +139,25 @@ __host__ __device__ constexpr int bindex(int b0, int b1, int b2, int mm) {
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+// L2 policy for the streamed targets (read once by TMA, written once): evict
+// first, so the source rows a neighbouring CTA row reads again stay in L2
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_global_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(__cvta_generic_to_global(p)), "d"(v), "l"(pol));
+}
+__device__ __forceinline__ void tma_box_hint(double* smem, const CUtensorMap* map, int x, int y, int layer, uint64_t* bar,
+                                             uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6], %7;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(0), "r"(layer),
+      "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))), "l"(pol)
+      : "memory");
 }
 __device__ __forceinline__ void st_global(double* p, double v) {
   asm volatile("st.global.f64 [%0], %1;\n" ::"l"(__cvta_generic_to_global(p)), "d"(v));
@@ -565,6 +587,10 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     cp_async_commit();
   };
 
+  // evict-first targets: velocity and V_z launches -1.5 %; the merged launch
+  // +1.5 % (kept on the default policy)
+  constexpr bool L2H = HLF_L2HINT && NT != 2;
+  const uint64_t l2pol = L2H ? evict_first_policy() : 0;
   // target boxes of layer kk into stage kk % TST (one per target field)
   auto issue_tgt = [&](int kk) {
     const int ts = kk % TST;
@@ -572,7 +598,8 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
     fence_proxy_async();
 #pragma unroll
     for (int t = 0; t < NTT; ++t)
-      tma_box(tgs + (ts * NTT + t) * F * TXC, &P.tmapT[t], x0, ty, P.t_zoff + kk, &tgtbar[ts]);
+      if (L2H) tma_box_hint(tgs + (ts * NTT + t) * F * TXC, &P.tmapT[t], x0, ty, P.t_zoff + kk, &tgtbar[ts], l2pol);
+      else tma_box(tgs + (ts * NTT + t) * F * TXC, &P.tmapT[t], x0, ty, P.t_zoff + kk, &tgtbar[ts]);
   };
   // iteration k0-1 is the prologue: it only builds ring layer k0.  The raw
   // layers k0 .. k0+RST-1 and the target layers k0 .. k0+TST-2 go out first.
@@ -677,7 +704,10 @@ __global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid
               const int df = (2 * a * n1 + 2 * b) * n1 + 2 * d;
               const double v = fma(acc[a][b][d], ix[a] * iy[b] * iz[d], tp[df * TXC]);
               emax = max(emax, __double2hiint(v) & 0x7fffffff);  // >= 0x7ff00000: inf / nan
-              if (zactive) st_global(dp + df * P.t_plane32, v);
+              if (zactive) {
+                if (L2H) st_global_hint(dp + df * P.t_plane32, v, l2pol);
+                else st_global(dp + df * P.t_plane32, v);
+              }
             }
           }
         }
