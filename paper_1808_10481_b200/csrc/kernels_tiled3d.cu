@@ -312,7 +312,10 @@ __device__ __forceinline__ void xy_merged(int px, const TParams& P, const double
 __device__ __forceinline__ double ifact_s(int o) { return o <= 1 ? 1.0 : (o == 2 ? 0.5 : 1.0 / 6.0); }
 
 template <int MM, int NT>
-__global__ void __launch_bounds__(NTHREADS, MM < 3 ? 2 : 1) tiled3d(const __grid_constant__ TParams P) {
+#ifndef HLF_M1_CTAS
+#define HLF_M1_CTAS 3  // m = 1: 3 CTAs per SM (<= 85 registers): 19.5 -> 17.8 ms at 512x512x256
+#endif
+__global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2 : 1)) tiled3d(const __grid_constant__ TParams P) {
   using G = Cfg<MM>;
   constexpr int n1 = G::n1, n = G::n, F = G::F, nh = G::nh, jh = G::jh;
   static_assert(nh == MM + 1, "n/2 == m+1");
