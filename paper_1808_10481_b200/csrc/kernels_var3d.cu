@@ -88,7 +88,10 @@ struct V3Params {
 };
 
 template <int MM, int KIND>
-__global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Params Q) {
+#ifndef HLF_V3_MINB
+#define HLF_V3_MINB 2  // 8 warps per SM with the unrolled line loops beat 16 register-capped ones: 4.9 -> 7.4e9 DOF/s at 192^3 m = 3
+#endif
+__global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_constant__ V3Params Q) {
   using C = V3<MM>;
   constexpr int n1 = C::n1, n = C::n, F = C::F, E = C::E, T = C::T;
   constexpr int NOUT = KIND == VEL ? 3 : 1;
@@ -185,7 +188,10 @@ __global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Pa
       double* out = Cb;
 #pragma unroll 1
       for (int ax = 0; ax < 3; ++ax) {
-        for (int l = lane; l < n * n; l += 32) {
+#pragma unroll
+        for (int it = 0; it < (n * n + 31) / 32; ++it) {
+          const int l = lane + 32 * it;
+          if (l >= n * n) break;
           int base, st;
           line_of<MM>(ax, l, base, st);
           double v[n];
@@ -215,7 +221,10 @@ __global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Pa
       for (int ax = 2; ax >= 0; --ax) {
         const double* s = ax == 0 ? sx : (ax == 1 ? sy : sz);  // compile-time after unrolling
         const double* in = ax == 2 ? X : B;
-        for (int l = lane; l < n * n; l += 32) {
+#pragma unroll
+        for (int it = 0; it < (n * n + 31) / 32; ++it) {
+          const int l = lane + 32 * it;
+          if (l >= n * n) break;
           int base, st;
           line_of<MM>(ax, l, base, st);
           double v[n];
@@ -236,6 +245,7 @@ __global__ void __launch_bounds__(WARPS * 32) var3d(const __grid_constant__ V3Pa
 
     // Y <- av Lap X (truncated second derivatives, jet_differentiate twice per axis)
     auto av_lap = [&](const double* X, double* Y) {
+#pragma unroll 4
       for (int e = lane; e < E; e += 32) {
         const int q[3] = {e / (n * n), (e / n) % n, e % n};
         double acc = 0.0;

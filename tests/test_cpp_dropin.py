@@ -11,6 +11,7 @@ import oracle as O
 
 EXE = os.path.join(O.HERE, "_ref", "test_b200_stepper1d")
 EXE2D = os.path.join(O.HERE, "_ref", "test_b200_stepper2d")
+EXESLABS = os.path.join(O.HERE, "_ref", "test_b200_slabs")
 
 
 @pytest.mark.gpu
@@ -35,6 +36,17 @@ def test_cpp_dropin_stepper2d_suite():
     if not os.path.exists(EXE2D):
         pytest.skip("2D drop-in test binary not built (needs /root/reference at build time)")
     r = subprocess.run([EXE2D], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "| 0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_host_slab_group():
+    # the multi-GPU z-slab path driven from C++ through the C-ABI only
+    if not os.path.exists(EXESLABS):
+        pytest.skip("slab-group test binary not built")
+    r = subprocess.run([EXESLABS], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "| 0 failed" in r.stdout
