@@ -162,12 +162,18 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
       }
 
     // ---- reconstruction of one source field into Cb (x, y, z sweeps of M)
-    auto reconstruct = [&](int comp) {
+    // gather of one source field's stacked corner tensor: this lane's E/32
+    // entries are loaded into registers first (gather_load, issued one
+    // component ahead so the loads overlap the previous component's sweeps)
+    // and stored to A later (gather_store)
+    constexpr int GL = (E + 31) / 32;
+    auto gather_load = [&](int comp, double (&g)[GL]) {
       const double* src = P.src[comp];
-#pragma unroll 4
-      for (int e = lane; e < E; e += 32) {
-        const int qx = e / (n * n), qy = (e / n) % n, qz = e % n;
-        const int q[3] = {qx, qy, qz};
+#pragma unroll
+      for (int j = 0; j < GL; ++j) {
+        const int e = lane + 32 * j;
+        if (e >= E) break;
+        const int q[3] = {e / (n * n), (e / n) % n, e % n};
         int f = 0;
         int64_t off = 0;
         double sign = 1.0;
@@ -181,8 +187,23 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
             if (comp != ax) sign = -sign;  // tangential velocity is odd across the wall
           }
         }
-        A[pidx<MM>(qx, qy, qz)] = sign * __ldg(src + off + static_cast<int64_t>(f) * P.s_coef);
+        g[j] = sign * __ldg(src + off + static_cast<int64_t>(f) * P.s_coef);
       }
+    };
+    auto gather_store = [&](const double (&g)[GL]) {
+#pragma unroll
+      for (int j = 0; j < GL; ++j) {
+        const int e = lane + 32 * j;
+        if (e >= E) break;
+        A[pidx<MM>(e / (n * n), (e / n) % n, e % n)] = g[j];
+      }
+    };
+    double gbuf[GL];
+    // ---- reconstruction of the gathered field (gbuf) into Cb (x, y, z sweeps
+    // of M); `next` >= 0 issues the gather of component `next` meanwhile
+    auto reconstruct = [&](int next) {
+      gather_store(gbuf);
+      if (next >= 0) gather_load(next, gbuf);
       __syncwarp();
       double* in = A;
       double* out = Cb;
@@ -268,9 +289,10 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
       double dsum[(E + 31) / 32];
 #pragma unroll
       for (int j = 0; j < (E + 31) / 32; ++j) dsum[j] = 0.0;
+      gather_load(0, gbuf);
 #pragma unroll 1
       for (int comp = 0; comp < NSRC; ++comp) {
-        reconstruct(comp);  // -> Cb
+        reconstruct(comp + 1 < NSRC ? comp + 1 : -1);  // -> Cb (gather of comp + 1 in flight)
 #pragma unroll
         for (int j = 0; j < (E + 31) / 32; ++j) {
           const int e = lane + 32 * j;
@@ -312,7 +334,8 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
         }
       }
     } else {
-      reconstruct(0);  // P_0 in Cb
+      gather_load(0, gbuf);
+      reconstruct(-1);  // P_0 in Cb
       double* Pc = Cb;
       double* Xs = A;
 #pragma unroll 1
