@@ -667,6 +667,36 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
       } else {
         cp_async_wait_group1();  // this lane's targets(k) landed; raw(k+2) may be in flight
       }
+      // velocity launch, m = 3: the three components' CK sums are one shared
+      // Q sum at shifted indices (v_c[o] = Q[o + e_c], GM does not depend on
+      // c; tiled3d_gen.cuh m3_vel_qs): 2624 instead of 3360 FMAs per cell,
+      // summed once per class before the epilogue (-1 %: the CK is not what
+      // bounds this launch)
+#ifndef HLF_VEL_PERCOMP
+      constexpr bool VQ = NT == 3 && MM == 3 && !V7;
+#else
+      constexpr bool VQ = false;
+#endif
+      double accq[VQ ? 3 : 1][jh][jh][jh];
+      if constexpr (VQ) {
+        // one body for every class, then each component takes its entries
+        // j + (1 - P_c) e_c (warp-uniform shifts).  Per-class bodies with
+        // only the entries a class needs (1884 FMAs per cell) ran 28 % slower:
+        // eight live code paths
+
+        double Q[jh + 1][jh + 1][jh + 1];
+        m3_vel_qs(P, pt, Q);
+#pragma unroll
+        for (int a = 0; a < jh; ++a)
+#pragma unroll
+          for (int b = 0; b < jh; ++b)
+#pragma unroll
+            for (int d = 0; d < jh; ++d) {
+              accq[VQ ? 0 : 0][a][b][d] = PX ? Q[a][b][d] : Q[a + 1][b][d];
+              accq[VQ ? 1 : 0][a][b][d] = PY ? Q[a][b][d] : Q[a][b + 1][d];
+              accq[VQ ? 2 : 0][a][b][d] = PZ ? Q[a][b][d] : Q[a][b][d + 1];
+            }
+      }
       // the velocity launch's three components unrolled (their CK chains
       // interleave: 66.2 -> 63.4 ms at 512x512x256)
 #pragma unroll
@@ -688,7 +718,14 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
         // TMA targets sit in stage k % TST; the lane-private cp.async path uses stage 0
         const double* tp = tgs + ((P.tma_t ? k % TST : 0) * NTT + t) * F * TXC + f0 * TXC + zcell;
 #ifndef HLF_EXP_NOCK
-        if constexpr (V7S) v7_zck(c, PX, PY, PZ, P, ro + cbase, rn + cbase, cz, zg, acc);
+        if constexpr (VQ) {
+#pragma unroll
+          for (int a = 0; a < jh; ++a)
+#pragma unroll
+            for (int b = 0; b < jh; ++b)
+#pragma unroll
+              for (int d = 0; d < jh; ++d) acc[a][b][d] = accq[VQ ? t : 0][a][b][d];
+        } else if constexpr (V7S) v7_zck(c, PX, PY, PZ, P, ro + cbase, rn + cbase, cz, zg, acc);
         else if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);
         else ck_any<MM>(c, warp, P, pt, acc);
 #else

@@ -22,6 +22,7 @@ Usage: python tools/gen_tiled3d.py   (writes the header; committed)
 """
 from __future__ import annotations
 
+import itertools
 import os
 
 TXC = 32
@@ -198,6 +199,33 @@ def ck_body(mm, c, cls):
     return outs, stm
 
 
+def gen_vel_q_shared(mm):
+    """Velocity launch, one CK body for every class: the Q entries any class
+    needs (class-local q in [0, jh]^3 with at most one coordinate = jh:
+    v_c[o] = Q[o + e_c] reads q = j + (1 - P_c) e_c), 2624 instead of 3360
+    FMAs per cell at m = 3; the class picks its three components' entries
+    (warp-uniform shifts) in m3_vel_pick."""
+    n1, n = mm + 1, 2 * mm + 2
+    nh, jh = n // 2, (n1 + 1) // 2
+    L = [f"__device__ __forceinline__ void m{mm}_vel_qs(const TParams& P, const double (&pt)[{nh}][{nh}][{nh}],",
+         f"    double (&Q)[{jh + 1}][{jh + 1}][{jh + 1}]) {{"]
+    for q in itertools.product(range(jh + 1), repeat=3):
+        if sum(1 for x in q if x == jh) > 1:
+            continue
+        nm = f"Q[{q[0]}][{q[1]}][{q[2]}]"
+        L.append(f"  {nm} = 0.0;")
+        for b0 in range(mm + 1):
+            for b1 in range(mm + 1 - b0):
+                for b2 in range(mm + 1 - b0 - b1):
+                    b = (b0, b1, b2)
+                    i = [q[a] + b[a] for a in range(3)]
+                    if any(x >= nh for x in i):
+                        continue
+                    L.append(f"  {nm} = fma(P.GM[{bindex(b, mm)}], pt[{i[0]}][{i[1]}][{i[2]}], {nm});")
+    L.append("}")
+    return "\n".join(L)
+
+
 def main():
     parts = ["// GENERATED by tools/gen_tiled3d.py -- do not edit.",
              "// Stage code of the tiled 3D Hermite-leapfrog kernel (kernels_tiled3d.cu).",
@@ -274,6 +302,9 @@ def main():
         parts.append("  }")
         parts.append("}")
         parts.append("")
+        if mm == 3:
+            parts.append(gen_vel_q_shared(mm))
+            parts.append("")
         parts.append(f"// m = {mm}: {len(bodies)} distinct CK bodies")
         parts.append("")
     with open(OUT, "w") as f:
