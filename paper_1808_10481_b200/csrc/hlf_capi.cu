@@ -305,7 +305,7 @@ void fill_weights(const hlf_solver* s, hlfk::HalfKind kind, HalfParams& P) {
 // var2d (2D with per-node ap jets)
 bool tiled_available(const hlf_solver* s) {
   if (!s->m_mirror) return false;
-  if (s->variable) return (s->d == 2 && hlfk::var2d_supported(s->m)) || (s->d == 3 && s->sep3d);
+  if (s->variable) return (s->d == 2 && hlfk::var2d_supported(s->m)) || (s->d == 3 && s->sep3d);  // sep3d: the coefficient lives in the kernel
   return (s->d == 3 && hlfk::tiled3d_supported(s->m)) || (s->d == 2 && hlfk::tiled2d_supported(s->m));
 }
 
@@ -370,12 +370,15 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
     P.tNz = zhi - zlo;
   }
   int launched = -1;
-  if (s->variant == 1 && s->variable && s->sep3d && s->d == 3) {
+  if (s->variable && s->sep3d) {
     // coordinates of target node 0 (primary: x_min, dual: x_min + h/2; z from the layer range)
-    double x0[3];
-    for (int ax = 0; ax < 3; ++ax) x0[ax] = s->x_min[ax] + (fg == HLF_DUAL ? 0.5 * s->h : 0.0);
-    x0[2] += zlo * s->h;
-    launched = hlfk::launch_half_var3d(s->m, kind, P, s->sep, x0, s->stream);
+    for (int ax = 0; ax < 3; ++ax) P.sep_x0[ax] = s->x_min[ax] + (fg == HLF_DUAL ? 0.5 * s->h : 0.0);
+    P.sep_x0[2] += zlo * s->h;
+    std::memcpy(P.sep, s->sep, sizeof(P.sep));
+    P.sep_on = 1;
+  }
+  if (s->variant == 1 && s->variable && s->sep3d && s->d == 3) {
+    launched = hlfk::launch_half_var3d(s->m, kind, P, s->sep, P.sep_x0, s->stream);
   } else if (s->variant == 1 && !s->variable && s->d == 3 && hlfk::tiled3d_supported(s->m))
     launched = hlfk::launch_half_tiled3d(s->m, kind, P, s->stream);
   else if (s->variant == 1 && !s->variable && s->d == 2 && hlfk::tiled2d_supported(s->m))
@@ -383,7 +386,8 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
   else if (s->variant == 1 && s->variable && s->d == 2 && hlfk::var2d_supported(s->m))
     launched = hlfk::launch_half_var2d(s->m, kind, P, s->stream);
   if (launched < 0 && s->variable && s->sep3d)
-    return fail(s, HLF_CONFIG_ERROR, "on-the-fly separable coefficients need the var3d kernel (variant 1, m <= 3)");
+    return fail(s, HLF_CONFIG_ERROR,
+                "on-the-fly separable coefficients need the var2d / var3d kernel (variant 1)");
   if (launched == -2 || launched < 0 && s->variant != 1)  // -2: custom M / planes too large for the tiled kernel
     launched = hlfk::launch_half_generic(s->d, s->m, s->variable, kind, P, s->stream);
   if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
@@ -578,6 +582,11 @@ hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets) {
     return fail(s, HLF_INVALID_ARGUMENT, "bad grid or buffer");
   if (!s->variable) return fail(s, HLF_CONFIG_ERROR, "solver was created with constant coefficients");
   cudaSetDevice(s->device);
+  if (s->sep3d) {
+    s->sep3d = false;  // back to stored jets
+    ++s->gen;
+    if (s->d == 3) s->variant = tiled_available(s) ? 1 : 0;
+  }
   const int* N = grid == HLF_PRIMARY ? s->Np : s->Nd;
   const int64_t plane = static_cast<int64_t>(N[0]) * N[1];
   if (!s->coeff[grid]) {
@@ -600,9 +609,9 @@ hlf_status hlf_set_coeff_separable(hlf_solver* s, double c0, double c1, const do
     s->sep[5 + a] = a < s->d ? phase[a] : 0.0;
   }
   ++s->gen;
-  if (s->d == 3 && hlfk::var3d_supported(s->m) && s->m_mirror) {
-    s->sep3d = true;  // generated inside the kernel: nothing stored
-    s->variant = 1;   // the var3d kernel (the generic kernel reads stored jets)
+  if (((s->d == 3 && hlfk::var3d_supported(s->m)) || (s->d == 2 && hlfk::var2d_supported(s->m))) && s->m_mirror) {
+    s->sep3d = true;  // generated inside the var3d / var2d kernel: nothing stored
+    s->variant = 1;   // (the generic kernel reads stored jets)
     return HLF_OK;
   }
   s->sep3d = false;

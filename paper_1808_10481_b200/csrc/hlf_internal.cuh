@@ -56,6 +56,11 @@ struct HalfParams {
   // recorded after the i-th kernel of this half step (launch_ev[0] before it)
   cudaEvent_t* launch_ev;
   int* launch_idx;
+  // separable coefficient generated in the kernel (var2d; var3d reads its own copy):
+  // ap = -(sep[0] + sep[1] prod sin(sep[2+a] x_a + sep[5+a])), sep_x0 = target node 0
+  int sep_on;
+  double sep[8];
+  double sep_x0[3];
 };
 
 // record the "after launch" event of a timed half step (no-op otherwise)

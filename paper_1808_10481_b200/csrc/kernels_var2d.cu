@@ -181,6 +181,76 @@ __device__ __forceinline__ void product(const double* A, const double* X, int t,
   product_ix<MM, KIND, K, 0>(A, X, t, acc);
 }
 
+// ---- separable coefficient (hlf_set_coeff_separable): ap = -c0 e_0 - c1 sx (x) sy,
+// so ap (.) X = -c0 X - c1 Sx(Sy(X)): Y = Sy(X) row by row (causal
+// convolution with sy along qy, thread-local), then each output row mixes the
+// rows below it with sx (all rows: Y goes through shared memory, buffer A)
+template <int MM, int KIND, int K, int J>
+__device__ __forceinline__ void sep_ysweep_row(const double (&sy)[2 * MM + 2], const double* X, double* Y, int t) {
+  using S = Shape<MM>;
+  constexpr int Lj = RowLim<MM, KIND, K, J>::v, last = RowLim<MM, KIND, K, J>::last;
+  if constexpr (Lj >= 0) {
+    const int r = 2 * J + t;
+    if (r <= last) {
+      double xv[S::n + 2], yv[S::n + 2];
+#pragma unroll
+      for (int i = 0; i <= Lj; i += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(X + r * S::RS + i);
+        xv[i] = v.x;
+        xv[i + 1] = v.y;
+      }
+#pragma unroll
+      for (int qy = 0; qy <= Lj; ++qy) {
+        double y = 0.0;
+#pragma unroll
+        for (int b = 0; b <= qy; ++b) y = fma(sy[b], xv[qy - b], y);
+        yv[qy] = y;
+      }
+      yv[Lj + 1] = 0.0;
+#pragma unroll
+      for (int i = 0; i <= Lj; i += 2) *reinterpret_cast<double2*>(Y + r * S::RS + i) = make_double2(yv[i], yv[i + 1]);
+    }
+  }
+}
+
+template <int MM, int KIND, int K, int J>
+__device__ __forceinline__ void sep_xcomb_row(const double (&nsx)[2 * MM + 2], double c0, const double* X,
+                                              const double* Y, int t, double (&acc)[MM + 1][2 * MM + 2]) {
+  using S = Shape<MM>;
+  constexpr int Lj = RowLim<MM, KIND, K, J>::v, last = RowLim<MM, KIND, K, J>::last;
+  if constexpr (Lj >= 0) {
+    const int r = 2 * J + t;
+    if (r <= last) {
+#pragma unroll
+      for (int i = 0; i <= Lj; i += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(X + r * S::RS + i);
+        acc[J][i] = -c0 * v.x;
+        if (i + 1 <= Lj) acc[J][i + 1 <= Lj ? i + 1 : i] = -c0 * v.y;
+      }
+#pragma unroll
+      for (int a = 0; a <= 2 * J + 1; ++a) {
+        if (a > r) break;
+        const double* yr = Y + (r - a) * S::RS;
+#pragma unroll
+        for (int i = 0; i <= Lj; i += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(yr + i);
+          acc[J][i] = fma(nsx[a], v.x, acc[J][i]);
+          if (i + 1 <= Lj) acc[J][i + 1 <= Lj ? i + 1 : i] = fma(nsx[a], v.y, acc[J][i + 1 <= Lj ? i + 1 : i]);
+        }
+      }
+    }
+  }
+}
+
+template <int MM, int KIND, int K, int... J>
+__device__ __forceinline__ void product_sep_(std::integer_sequence<int, J...>, const double (&nsx)[2 * MM + 2],
+                                             const double (&sy)[2 * MM + 2], double c0, double* A, const double* X,
+                                             int t, double (&acc)[MM + 1][2 * MM + 2]) {
+  (sep_ysweep_row<MM, KIND, K, J>(sy, X, A, t), ...);
+  __syncwarp();
+  (sep_xcomb_row<MM, KIND, K, J>(nsx, c0, X, A, t, acc), ...);
+}
+
 // X_K = av Lap P_{K-2} on thread-row J (row r + 2 = acc[J + 1])
 template <int MM, int KIND, int K, int J>
 __device__ __forceinline__ void lap_row(double (&acc)[MM + 1][2 * MM + 2], int t, double c) {
@@ -229,12 +299,30 @@ __device__ __forceinline__ void laplacian_store(double (&acc)[MM + 1][2 * MM + 2
   laplacian_store_<MM, KIND, K>(std::make_integer_sequence<int, MM + 1>{}, acc, X, t, c);
 }
 
+// the ap operand: stored jets in A (SEP = false) or the separable data
+template <int MM, bool SEP>
+struct Coef {
+  double* A;                // stored jet rows (SEP: scratch for Sy(X))
+  double nsx[2 * MM + 2];   // -c1 sx (SEP)
+  double sy[2 * MM + 2];    // sy (SEP)
+  double c0;
+};
+
+template <int MM, int KIND, int K, bool SEP>
+__device__ __forceinline__ void product_any(Coef<MM, SEP>& C, const double* X, int t,
+                                            double (&acc)[MM + 1][2 * MM + 2]) {
+  if constexpr (SEP)
+    product_sep_<MM, KIND, K>(std::make_integer_sequence<int, MM + 1>{}, C.nsx, C.sy, C.c0, C.A, X, t, acc);
+  else
+    product<MM, KIND, K>(C.A, X, t, acc);
+}
+
 // PRE levels K = 1, 3, .., n - 1: P_K = ap (.) X_K, target += w_K P_K,
 // X_{K+2} = av Lap P_K
-template <int MM, int K>
-__device__ __forceinline__ void pre_levels(const HalfParams& P, const double* A, double* X, int t, double c,
+template <int MM, int K, bool SEP>
+__device__ __forceinline__ void pre_levels(const HalfParams& P, Coef<MM, SEP>& A, double* X, int t, double c,
                                            double (&acc)[MM + 1][2 * MM + 2], double (&tgt)[MM / 2 + 1][MM + 1]) {
-  product<MM, PRE, K>(A, X, t, acc);
+  product_any<MM, PRE, K>(A, X, t, acc);
 #pragma unroll
   for (int s = 0; s <= MM / 2; ++s)
     if (2 * s + t <= MM) {
@@ -243,15 +331,15 @@ __device__ __forceinline__ void pre_levels(const HalfParams& P, const double* A,
     }
   if constexpr (K + 2 < 2 * MM + 2) {
     laplacian_store<MM, PRE, K + 2>(acc, X, t, c);
-    pre_levels<MM, K + 2>(P, A, X, t, c, acc, tgt);
+    pre_levels<MM, K + 2, SEP>(P, A, X, t, c, acc, tgt);
   }
 }
 
 // VEL levels K = 0, 2, .., n - 2: target_c += w_{K+1} av d_c P_K on the
 // target rows (d_x reads row r + 1, the partner's), then X_{K+2} = av Lap P_K
 // and P_{K+2} = ap (.) X_{K+2}
-template <int MM, int K>
-__device__ __forceinline__ void vel_levels(const HalfParams& P, const double* A, double* X, int t, double c,
+template <int MM, int K, bool SEP>
+__device__ __forceinline__ void vel_levels(const HalfParams& P, Coef<MM, SEP>& A, double* X, int t, double c,
                                            double inv_h, double (&acc)[MM + 1][2 * MM + 2],
                                            double (&tgt)[2][MM / 2 + 1][MM + 1]) {
   constexpr int NJ = MM + 1;
@@ -272,12 +360,12 @@ __device__ __forceinline__ void vel_levels(const HalfParams& P, const double* A,
   }
   if constexpr (K + 2 < 2 * MM + 1) {
     laplacian_store<MM, VEL, K + 2>(acc, X, t, c);
-    product<MM, VEL, K + 2>(A, X, t, acc);
-    vel_levels<MM, K + 2>(P, A, X, t, c, inv_h, acc, tgt);
+    product_any<MM, VEL, K + 2>(A, X, t, acc);
+    vel_levels<MM, K + 2, SEP>(P, A, X, t, c, inv_h, acc, tgt);
   }
 }
 
-template <int MM, int KIND>
+template <int MM, int KIND, bool SEP>
 __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfParams P) {
   using S = Shape<MM>;
   constexpr int n1 = S::n1, n = S::n, NJ = S::NJ, NS = S::NS;
@@ -298,8 +386,32 @@ __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfPa
   const int ty = live ? static_cast<int>(cell / P.tNx) : 0;
   const int64_t tnode = static_cast<int64_t>(ty) * P.tNx + tx;
 
-  // ap jet rows t, t + 2, .. -> A  ([E][y][x] planes, e = qx n + qy)
-  {
+  Coef<MM, SEP> coef;
+  coef.A = A;
+  if constexpr (SEP) {
+    // ap = -(c0 + c1 sin(w_x x + ph_x) sin(w_y y + ph_y)) at the target node:
+    // the reference's sin_jet (jet.cpp:65-74) per axis
+    const double xx = P.sep_x0[0] + tx * P.h, yy = P.sep_x0[1] + ty * P.h;
+    double sn, cs;
+    sincos(P.sep[2] * xx + P.sep[5], &sn, &cs);
+    double f = 1.0;
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const int r4 = k & 3;
+      coef.nsx[k] = -P.sep[1] * f * (r4 == 0 ? sn : (r4 == 1 ? cs : (r4 == 2 ? -sn : -cs)));
+      f = f * (P.sep[2] * P.h) / (k + 1);
+    }
+    sincos(P.sep[3] * yy + P.sep[6], &sn, &cs);
+    f = 1.0;
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const int r4 = k & 3;
+      coef.sy[k] = f * (r4 == 0 ? sn : (r4 == 1 ? cs : (r4 == 2 ? -sn : -cs)));
+      f = f * (P.sep[3] * P.h) / (k + 1);
+    }
+    coef.c0 = P.sep[0];
+  } else {
+    // ap jet rows t, t + 2, .. -> A  ([E][y][x] planes, e = qx n + qy)
     const double* ap = P.coeff + tnode;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
@@ -441,9 +553,9 @@ __global__ void __launch_bounds__(NTHREADS) var2d(const __grid_constant__ HalfPa
       }
     }
     __syncwarp();
-    pre_levels<MM, 1>(P, A, X, t, lap_c, acc, tgt[0]);
+    pre_levels<MM, 1, SEP>(P, coef, X, t, lap_c, acc, tgt[0]);
   } else {
-    vel_levels<MM, 0>(P, A, X, t, lap_c, inv_h, acc, tgt);
+    vel_levels<MM, 0, SEP>(P, coef, X, t, lap_c, inv_h, acc, tgt);
   }
 
   // in-place store + finite flag (check_finite, stepper1d.cpp:121-129)
@@ -470,13 +582,22 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(p.tNx) * p.tNy;
   const int64_t blocks = (total + S::CPC - 1) / S::CPC;
   if (blocks > 0x7fffffff) return -2;
-  static std::atomic<unsigned long long> vel_ok{0}, pre_ok{0};
-  if (kind == VEL) ensure_smem_opt_in(var2d<MM, VEL>, S::SMEM, vel_ok);
-  else ensure_smem_opt_in(var2d<MM, PRE>, S::SMEM, pre_ok);
+  static std::atomic<unsigned long long> vel_ok{0}, pre_ok{0}, vel_sep{0}, pre_sep{0};
+  if (p.sep_on) {
+    if (kind == VEL) ensure_smem_opt_in(var2d<MM, VEL, true>, S::SMEM, vel_sep);
+    else ensure_smem_opt_in(var2d<MM, PRE, true>, S::SMEM, pre_sep);
+    if (kind == VEL)
+      var2d<MM, VEL, true><<<static_cast<unsigned>(blocks), NTHREADS, S::SMEM, st>>>(p);
+    else
+      var2d<MM, PRE, true><<<static_cast<unsigned>(blocks), NTHREADS, S::SMEM, st>>>(p);
+    return 1;
+  }
+  if (kind == VEL) ensure_smem_opt_in(var2d<MM, VEL, false>, S::SMEM, vel_ok);
+  else ensure_smem_opt_in(var2d<MM, PRE, false>, S::SMEM, pre_ok);
   if (kind == VEL)
-    var2d<MM, VEL><<<static_cast<unsigned>(blocks), NTHREADS, S::SMEM, st>>>(p);
+    var2d<MM, VEL, false><<<static_cast<unsigned>(blocks), NTHREADS, S::SMEM, st>>>(p);
   else
-    var2d<MM, PRE><<<static_cast<unsigned>(blocks), NTHREADS, S::SMEM, st>>>(p);
+    var2d<MM, PRE, false><<<static_cast<unsigned>(blocks), NTHREADS, S::SMEM, st>>>(p);
   return 1;
 }
 

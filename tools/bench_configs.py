@@ -4,7 +4,8 @@ The headline 3D line is bench.py's; this script records the others:
 
   cfg1   1D m=3 standing wave, K=256 (143 steps) and K=2^24
   cfg2   2D periodic acoustics mode, K=1024, m=1..4 (+ 4096^2 m=3)
-  cfg3   2D walls, K=4096, m=3, c^2 = 1 + sin(pi x) sin(pi y)/2 jets (var2d kernel;
+  cfg3   2D walls, K=4096, m=3, c^2 = 1 + sin(pi x) sin(pi y)/2 generated in the
+         var2d kernel (hlf_set_coeff_separable; and as stored jets, hlf_set_coeff;
          separable data instead of the Gaussian pulse: same arithmetic)
   cfg4   3D periodic, 512x512x256, m=1..3 (bench.py's workload)
   cfg3-3D  3D periodic, 192^3, m=1..3, c^2 = 1 + sin(pi x) sin(pi y) sin(pi z)/2
@@ -117,7 +118,8 @@ def main():
     for m in (1, 2, 3, 4):
         res.append(run("cfg2", 2, m, [1024, 1024], steps=100))
     res.append(run("cfg2 large", 2, 3, [4096, 4096], steps=20))
-    res.append(run("cfg3", 2, 3, [4096, 4096], boundary=[1, 1], variable=True, steps=3))
+    res.append(run("cfg3", 2, 3, [4096, 4096], boundary=[1, 1], variable=True, separable=True, steps=3))
+    res.append(run("cfg3 stored jets", 2, 3, [4096, 4096], boundary=[1, 1], variable=True, steps=3))
     for m in (1, 2, 3):
         res.append(run("cfg4", 3, m, [512, 512, 256], steps=5))
     for m in (1, 2, 3):
