@@ -127,15 +127,18 @@ hlf_status hlf_set_coeff(hlf_solver* s, int grid, const double* host_jets);
    coefficient grids, 24 B per DOF-update); otherwise they are written to the
    per-node jet storage on the device.  Needs desc.variable_ap = 1. */
 hlf_status hlf_set_coeff_separable(hlf_solver* s, double c0, double c1, const double* w, const double* phase);
-/* 1D forcing (ck_recurrence_variable's z, stepper1d.cpp:22-38): the table for
+/* Forcing (ck_recurrence_variable's z, stepper1d.cpp:22-38): the table for
    the NEXT half step that updates `grid` (HLF_PRIMARY: hlf_advance_p, evaluated
    by the reference at (primary x_j, t_v); HLF_DUAL: hlf_advance_v, at (dual x_j,
-   t_p after the pressure half step)).  Host AoS [node][r][s], r = 0..2m
-   (levels z(r) of forcing_at), s = 0..2m+1 (the jet), i.e. (2m+1)(2m+2)
-   doubles per node.  Once a table has been set the solver is in forcing mode:
-   every half step needs a fresh table for its grid (HLF_CONFIG_ERROR
-   otherwise, so hlf_advance_n runs at most one step); hlf_clear_forcing leaves
-   forcing mode.  d = 1, leapfrog scheme only. */
+   t_p after the pressure half step)).  Host AoS [node][r][e], r = 0..2m
+   (levels z(r) of forcing_at), e = the n^d entries of the scaled tensor jet
+   (x-major, n = 2m+2; d = 1: the reference's Jet), i.e. (2m+1) n^d doubles
+   per node; z(r) is added to every level of the P table (p_t = ap div v + f).
+   Once a table has been set the solver is in forcing mode: every half step
+   needs a fresh table for its grid (HLF_CONFIG_ERROR otherwise, so
+   hlf_advance_n runs at most one step); hlf_clear_forcing leaves forcing
+   mode.  Leapfrog scheme; d > 1 runs the faithful generic kernel (separable
+   on-the-fly coefficients are expanded to stored jets). */
 hlf_status hlf_set_forcing(hlf_solver* s, int grid, const double* host_table);
 hlf_status hlf_clear_forcing(hlf_solver* s);
 hlf_status hlf_set_times(hlf_solver* s, double t_p, double t_v, double dt);

@@ -125,6 +125,7 @@ def orc_lib(fma: bool = False):
         L.orc_set_field.argtypes = [C.c_void_p, C.c_int, _dp]
         L.orc_get_field.argtypes = [C.c_void_p, C.c_int, _dp]
         L.orc_set_coeff.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp]
+        L.orc_set_forcing.argtypes = [C.c_void_p, C.c_int, _dp]
         L.orc_set_times.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
         L.orc_get_times.argtypes = [C.c_void_p, _dp]
         L.orc_advance_p.argtypes = [C.c_void_p]
@@ -355,6 +356,16 @@ class OracleStepper:
         jets = np.ascontiguousarray(jets, dtype=np.float64).ravel()
         assert jets.size == self.num_nodes(grid) * self.E
         self.L.orc_set_coeff(self.h_, grid, which, _ptr(jets))
+
+    def set_forcing(self, grid: int, table):
+        """forcing levels z(r) for the half steps updating `grid`:
+        [nodes, 2m+1, n^d] (hlf_set_forcing's table); None clears"""
+        if table is None:
+            self.L.orc_set_forcing(self.h_, grid, None)
+            return
+        table = np.ascontiguousarray(table, dtype=np.float64).ravel()
+        assert table.size == self.num_nodes(grid) * (2 * self.m + 1) * self.E
+        self.L.orc_set_forcing(self.h_, grid, _ptr(table))
 
     def set_M(self, M):
         M = np.ascontiguousarray(M, dtype=np.float64).ravel()

@@ -106,6 +106,7 @@ struct Oracle {
   std::vector<double> p;            // [primary node][F]
   std::vector<double> v[3];         // [dual node][F]
   std::vector<double> cj[2][2];     // [grid][ap/av] per-node n^d jets (empty = constant)
+  std::vector<double> fz[2];        // [grid] forcing levels z(r), [node][r = 0..n-2][n^d] (empty = none)
   // z-slab mode (d = 3, periodic z across ranks): z neighbours beyond the slab
   // come from halo layers set by the caller, [ix][iy][F]
   bool slab = false;
@@ -261,6 +262,10 @@ struct Oracle {
     }
   }
 
+  const double* forcing(int grid, size_t node) const {
+    return fz[grid].empty() ? nullptr : fz[grid].data() + node * static_cast<size_t>(n - 1) * E;
+  }
+
   const double* coeff(int grid, int which, size_t node) const {
     const auto& c = cj[grid][which];
     return c.empty() ? nullptr : c.data() + node * E;
@@ -268,8 +273,10 @@ struct Oracle {
 
   // one CK iteration level, both tables (stepper1d.cpp:22-38 generalized):
   // P[r+1] = ap (.) sum_c d_c V_c[r];  V_c[r+1] = av (.) d_c P[r]
+  // With a forcing table zt (the node's levels z(r), stepper1d.cpp:29-32)
+  // z(r) is added to P[r+1] after the product, as the reference does.
   void ck(std::vector<std::vector<double>>& P, std::vector<std::vector<double>> (&V)[3],
-          const double* apj, const double* avj) const {
+          const double* apj, const double* avj, const double* zt = nullptr) const {
     std::vector<double> tmp(E), acc(E);
     for (int r = 0; r + 1 < n; ++r) {
       for (int e = 0; e < E; ++e) acc[e] = 0.0;
@@ -282,6 +289,8 @@ struct Oracle {
       } else {
         for (int e = 0; e < E; ++e) P[r + 1][e] = ap * acc[e];
       }
+      if (zt)
+        for (int e = 0; e < E; ++e) P[r + 1][e] += zt[static_cast<size_t>(r) * E + e];
       for (int c = 0; c < d; ++c) {
         tensor_d(P[r].data(), c, tmp.data());
         if (avj) {
@@ -315,7 +324,7 @@ struct Oracle {
         }
         reconstruct(cp.data(), V[c][0].data());
       }
-      ck(P, V, coeff(0, 0, node), coeff(0, 1, node));
+      ck(P, V, coeff(0, 0, node), coeff(0, 1, node), forcing(0, node));
       leapfrog(p.data() + static_cast<size_t>(node) * F, P);
     }
     t_p += dt;
@@ -345,7 +354,7 @@ struct Oracle {
       std::vector<std::vector<double>> V[3];
       for (int c = 0; c < d; ++c) V[c].assign(n, std::vector<double>(E, 0.0));
       reconstruct(cp.data(), P[0].data());
-      ck(P, V, coeff(1, 0, node), coeff(1, 1, node));
+      ck(P, V, coeff(1, 0, node), coeff(1, 1, node), forcing(1, node));
       for (int c = 0; c < d; ++c) leapfrog(v[c].data() + static_cast<size_t>(node) * F, V[c]);
     }
     t_v += dt;
@@ -436,6 +445,17 @@ void orc_set_coeff(void* h, int grid, int which, const double* jets) {
     return;
   }
   c.assign(jets, jets + o->nodes(grid) * o->E);
+}
+
+// forcing levels for the half steps updating `grid` (0 primary, 1 dual):
+// [node][r = 0..2m][n^d]; null clears (hlf_set_forcing's table)
+void orc_set_forcing(void* h, int grid, const double* table) {
+  auto* o = static_cast<Oracle*>(h);
+  if (!table) {
+    o->fz[grid].clear();
+    return;
+  }
+  o->fz[grid].assign(table, table + o->nodes(grid) * static_cast<size_t>(o->n - 1) * o->E);
 }
 
 void orc_set_times(void* h, double t_p, double t_v, double dt) {

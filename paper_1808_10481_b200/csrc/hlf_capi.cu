@@ -357,6 +357,7 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
                   "forcing mode: set this half step's table with hlf_set_forcing (or hlf_clear_forcing)");
     P.force = s->force[fg];
     P.f_coef = s->plane[tf];
+    P.f_layer = s->plane[tf] * (s->n - 1) * s->E;
   }
   if (zhi < 0) zhi = P.tNz;
   if (zlo < 0 || zhi > P.tNz || zlo > zhi || (s->d != 3 && (zlo != 0 || zhi != P.tNz)))
@@ -366,6 +367,7 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
     for (int c = 0; c < 3; ++c)
       if (P.src[c]) P.src[c] += static_cast<int64_t>(zlo) * P.s_layer;
     if (P.coeff) P.coeff += static_cast<int64_t>(zlo) * P.c_layer;
+    if (P.force) P.force += static_cast<int64_t>(zlo) * P.f_layer;
     P.t_zoff += zlo;
     P.tNz = zhi - zlo;
   }
@@ -377,7 +379,9 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
     std::memcpy(P.sep, s->sep, sizeof(P.sep));
     P.sep_on = 1;
   }
-  if (s->variant == 1 && s->variable && s->sep3d && s->d == 3) {
+  if (P.force) {
+    // forced half steps: the faithful kernels (the tiled / var kernels have no forcing term)
+  } else if (s->variant == 1 && s->variable && s->sep3d && s->d == 3) {
     launched = hlfk::launch_half_var3d(s->m, kind, P, s->sep, P.sep_x0, s->stream);
   } else if (s->variant == 1 && !s->variable && s->d == 3 && hlfk::tiled3d_supported(s->m))
     launched = hlfk::launch_half_tiled3d(s->m, kind, P, s->stream);
@@ -388,7 +392,7 @@ hlf_status launch_half(hlf_solver* s, hlfk::HalfKind kind, int step, int zlo = 0
   if (launched < 0 && s->variable && s->sep3d)
     return fail(s, HLF_CONFIG_ERROR,
                 "on-the-fly separable coefficients need the var2d / var3d kernel (variant 1)");
-  if (launched == -2 || launched < 0 && s->variant != 1)  // -2: custom M / planes too large for the tiled kernel
+  if (launched == -2 || launched < 0 && (s->variant != 1 || P.force))  // -2: custom M / planes too large for the tiled kernel
     launched = hlfk::launch_half_generic(s->d, s->m, s->variable, kind, P, s->stream);
   if (launched < 0) return fail(s, HLF_CONFIG_ERROR, "no device kernel for this (dim, m)");
   if (s->timing && s->tev_idx == 0) mark_launch(P, s->stream);  // kernels without their own marks
@@ -609,7 +613,8 @@ hlf_status hlf_set_coeff_separable(hlf_solver* s, double c0, double c1, const do
     s->sep[5 + a] = a < s->d ? phase[a] : 0.0;
   }
   ++s->gen;
-  if (((s->d == 3 && hlfk::var3d_supported(s->m)) || (s->d == 2 && hlfk::var2d_supported(s->m))) && s->m_mirror) {
+  if (((s->d == 3 && hlfk::var3d_supported(s->m)) || (s->d == 2 && hlfk::var2d_supported(s->m))) && s->m_mirror &&
+      !s->force_on) {
     s->sep3d = true;  // generated inside the var3d / var2d kernel: nothing stored
     s->variant = 1;   // (the generic kernel reads stored jets)
     return HLF_OK;
@@ -633,11 +638,26 @@ hlf_status hlf_set_coeff_separable(hlf_solver* s, double c0, double c1, const do
 hlf_status hlf_set_forcing(hlf_solver* s, int grid, const double* host_table) {
   if (!s || (grid != HLF_PRIMARY && grid != HLF_DUAL) || !host_table)
     return fail(s, HLF_INVALID_ARGUMENT, "bad grid or buffer");
-  if (s->d != 1 || s->scheme != HLF_SCHEME_LEAPFROG)
-    return fail(s, HLF_CONFIG_ERROR, "forcing tables are supported for the 1D leapfrog scheme");
+  if (s->scheme != HLF_SCHEME_LEAPFROG)
+    return fail(s, HLF_CONFIG_ERROR, "forcing tables are supported for the leapfrog scheme");
   cudaSetDevice(s->device);
+  if (s->sep3d) {
+    // forced runs go through the generic kernel, which reads stored ap jets
+    s->sep3d = false;
+    for (int g = 0; g < 2; ++g) {
+      const int* Ng = g == HLF_PRIMARY ? s->Np : s->Nd;
+      if (!s->coeff[g]) {
+        const size_t bytes = static_cast<size_t>(s->num_nodes(g)) * s->E * sizeof(double);
+        HLF_CUDA(s, cudaMalloc(&s->coeff[g], bytes));
+      }
+      double x0[3];
+      for (int a = 0; a < 3; ++a) x0[a] = s->x_min[a] + (g == HLF_DUAL ? 0.5 * s->h : 0.0);
+      hlfk::launch_fill_sep_coeff(s->coeff[g], s->d, Ng, s->n, s->h, x0, s->sep, s->stream);
+      HLF_CUDA(s, cudaGetLastError());
+    }
+  }
   const int* N = grid == HLF_PRIMARY ? s->Np : s->Nd;
-  const int per = (s->n - 1) * s->n;
+  const int per = (s->n - 1) * s->E;
   if (!s->force[grid]) {
     const size_t bytes = static_cast<size_t>(s->num_nodes(grid)) * per * sizeof(double);
     HLF_CUDA(s, cudaMalloc(&s->force[grid], bytes));

@@ -39,8 +39,9 @@ struct HalfParams {
   int64_t s_layer, s_coef;      // source strides (elements)
   int64_t t_layer, t_coef;      // target strides
   int64_t c_layer, c_coef;      // coefficient-jet strides
-  const double* force;          // 1D forcing table z_r[s] at the target nodes, [(r n + s)][x], or null
-  int64_t f_coef;
+  const double* force;          // forcing table z_r at the target nodes, [z][(r n^d + e)][y][x], or null
+  int64_t f_coef;               // plane of the target grid
+  int64_t f_layer;              // (n - 1) n^d planes
   int sNx, sNy;                 // source plane size
   int tNx, tNy, tNz;            // target nodes to update
   int t_zoff;                   // layer index of target z = 0 (p: 0, v: 1)

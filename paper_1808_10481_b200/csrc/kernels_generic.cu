@@ -70,7 +70,10 @@ __device__ __forceinline__ int excess(int e) {
   return x;
 }
 
-template <int D, int MM, bool VAR, int KIND>
+// FRC: a forcing table z_r (n^d jets, levels r = 0..2m) at the target nodes is
+// added to every P level (ck_recurrence_variable's z, stepper1d.cpp:29-32,
+// generalised to tensor jets): both tables are then live at every level.
+template <int D, int MM, bool VAR, int KIND, bool FRC = false>
 __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ HalfParams P) {
   constexpr int n1 = MM + 1, n = 2 * MM + 2;
   constexpr int F = cpow(n1, D), E = cpow(n, D);
@@ -132,6 +135,15 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
   double Pt[E];
   double Vt[D * E];
   bool bad = false;
+  if constexpr (FRC) {  // the seeded-zero table is read at level 0 (ck_recurrence_variable: P[0] / V[0])
+#pragma unroll 1
+    for (int e = 0; e < E; ++e) {
+      if (KIND == VEL)
+        for (int c = 0; c < D; ++c) Vt[c * E + e] = 0.0;
+      else
+        Pt[e] = 0.0;
+    }
+  }
 
 #pragma unroll 1
   for (int comp = 0; comp < NSRC; ++comp) {
@@ -200,11 +212,30 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
 #pragma unroll 1
     for (int e = 0; e < E; ++e) apl[e] = __ldg(apj + e * P.c_coef);
   }
+  // forcing table of this node: [t_z][(r E + e)][t_y][t_x] (no ghost layers)
+  const double* zf = FRC ? P.force + static_cast<int64_t>(D == 3 ? t[2] : 0) * P.f_layer +
+                               static_cast<int64_t>(D >= 2 ? t[1] : 0) * P.tNx + t[0]
+                         : nullptr;
 #pragma unroll 1
   for (int r = 0; r + 1 < n; ++r) {
     const bool p_live = (KIND == VEL) == (r % 2 == 0);
     const int keep = n - 2 - r;  // level r + 1 entries with excess <= keep are read later
-    if (p_live) {
+    if (FRC) {
+      // both tables from level r: S = sum_c d_c V_c[r] first (old V), then
+      // V_c[r+1] = av d_c P[r] (old P), then P[r+1] = ap (.) S + z_r
+#pragma unroll 1
+      for (int e = 0; e < E; ++e) S[e] = 0.0;
+#pragma unroll 1
+      for (int c = 0; c < D; ++c) {
+        const int stride = cpow(n, D - 1 - c);
+#pragma unroll 1
+        for (int e = 0; e < E; ++e) {
+          if (excess<D, MM>(e) > keep) continue;
+          const int qc = (e / stride) % n;
+          const double dv = qc + 1 < n ? div_h(__dmul_rn(Vt[c * E + e + stride], static_cast<double>(qc + 1)), P) : 0.0;
+          S[e] = __dadd_rn(S[e], dv);
+        }
+      }
 #pragma unroll 1
       for (int c = 0; c < D; ++c) {
         const int stride = cpow(n, D - 1 - c);
@@ -216,12 +247,28 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
           Vt[c * E + e] = __dmul_rn(P.av, dv);
         }
       }
-    } else {
-      // Pt <- ap (.) (sum_c d_c V_c); the sum goes through S as scratch
-#pragma unroll 1
-      for (int e = 0; e < E; ++e) S[e] = 0.0;
+    }
+    if (FRC) {
+      // P[r+1] below (the p_live = false branch) from S
+    } else if (p_live) {
 #pragma unroll 1
       for (int c = 0; c < D; ++c) {
+        const int stride = cpow(n, D - 1 - c);
+#pragma unroll 1
+        for (int e = 0; e < E; ++e) {
+          if (excess<D, MM>(e) > keep) continue;
+          const int qc = (e / stride) % n;
+          const double dv = qc + 1 < n ? div_h(__dmul_rn(Pt[e + stride], static_cast<double>(qc + 1)), P) : 0.0;
+          Vt[c * E + e] = __dmul_rn(P.av, dv);
+        }
+      }
+    }
+    if (FRC || !p_live) {
+      // Pt <- ap (.) (sum_c d_c V_c); the sum goes through S as scratch
+#pragma unroll 1
+      for (int e = 0; e < E && !FRC; ++e) S[e] = 0.0;
+#pragma unroll 1
+      for (int c = 0; c < D && !FRC; ++c) {
         const int stride = cpow(n, D - 1 - c);
 #pragma unroll 1
         for (int e = 0; e < E; ++e) {
@@ -267,6 +314,11 @@ __global__ void __launch_bounds__(128) half_generic(const __grid_constant__ Half
 #pragma unroll 1
         for (int e = 0; e < E; ++e)
           if (excess<D, MM>(e) <= keep) Pt[e] = __dmul_rn(P.ap, S[e]);
+      }
+      if (FRC) {
+#pragma unroll 1
+        for (int e = 0; e < E; ++e)
+          if (excess<D, MM>(e) <= keep) Pt[e] = __dadd_rn(Pt[e], __ldg(zf + (r * E + e) * P.f_coef));
       }
     }
     // leapfrog_half_update (stepper1d.cpp:54-61): odd levels of the target's table
@@ -471,6 +523,16 @@ int launch_dm(bool variable, HalfKind kind, const HalfParams& p, cudaStream_t st
     } else {
       if (variable) half_1d<MM, true, PRE><<<blocks, threads, 0, st>>>(p);
       else half_1d<MM, false, PRE><<<blocks, threads, 0, st>>>(p);
+    }
+    return 1;
+  }
+  if (p.force) {
+    if (kind == VEL) {
+      if (variable) half_generic<D, MM, true, VEL, true><<<blocks, threads, 0, st>>>(p);
+      else half_generic<D, MM, false, VEL, true><<<blocks, threads, 0, st>>>(p);
+    } else {
+      if (variable) half_generic<D, MM, true, PRE, true><<<blocks, threads, 0, st>>>(p);
+      else half_generic<D, MM, false, PRE, true><<<blocks, threads, 0, st>>>(p);
     }
     return 1;
   }

@@ -299,11 +299,12 @@ class Stepper:
         self._c(self._L.hlf_set_coeff_separable(self._h, c0, c1, w3, p3))
 
     def set_forcing(self, grid: int, table: np.ndarray):
-        """1D forcing jets z_r (r = 0..2m, each 2m+2 long) at every node of
-        `grid` for the next half step updating that grid (hlf_set_forcing:
-        PRIMARY -> advance_p at t_v, DUAL -> advance_v at t_p)."""
+        """forcing jets z_r (r = 0..2m, each an n^d tensor jet, x-major) at
+        every node of `grid` for the next half step updating that grid
+        (hlf_set_forcing: PRIMARY -> advance_p at t_v, DUAL -> advance_v at
+        t_p): [nodes, 2m+1, n^d].  d > 1 runs the faithful generic kernel."""
         a = np.ascontiguousarray(table, dtype=np.float64)
-        if a.size != self.num_nodes(grid) * (self.n - 1) * self.n:
+        if a.size != self.num_nodes(grid) * (self.n - 1) * self.E:
             raise ValueError("forcing table has the wrong size")
         self._c(self._L.hlf_set_forcing(self._h, grid, a.ctypes.data))
 

@@ -329,8 +329,12 @@ def test_forcing_mode_needs_a_table_per_half_step():
     g.clear_forcing()
     g.advance_n(2)
     g2 = H.Stepper(H.Grid([-1.0] * 2, 0.2, (10, 10)), 2)
+    with pytest.raises(ValueError):
+        g2.set_forcing(H.PRIMARY, np.zeros((100, 5, 6)))  # 2D tables hold n^2 jets
+    g2.set_forcing(H.PRIMARY, np.zeros((100, 5, 36)))
+    g3 = H.Stepper(H.Grid([-1.0], 0.2, (10,)), 2, scheme=H.SCHEME_MODIFIED)
     with pytest.raises(H.ConfigError):
-        g2.set_forcing(H.PRIMARY, np.zeros((100, 5, 6)))
+        g3.set_forcing(H.PRIMARY, np.zeros((10, 5, 6)))  # leapfrog scheme only
 
 
 @pytest.mark.parametrize("d", [1, 2, 3])
