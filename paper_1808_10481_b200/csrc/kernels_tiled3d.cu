@@ -64,11 +64,15 @@ struct Cfg {
   static constexpr int RAWS = (RAW + 2 + 15) / 16 * 16;
   static constexpr int RING = n * n * n1 * TXC;
   // NT: 3 = velocity half (three targets), 1 = one pressure divergence term,
-  // 2 = merged V_x + V_y pressure launch (two raw sources, one target)
+  // 2 = merged V_x + V_y pressure launch (two raw sources, one target),
+  // 4 = the whole pressure half step (V_x + V_y merged as for 2, V_z in a
+  // second ring; three raw sources, one target)
   template <int NT>
-  static constexpr int NTGT = NT == 2 ? 1 : NT;
+  static constexpr int NTGT = NT == 2 || NT == 4 ? 1 : NT;
   template <int NT>
-  static constexpr int NSRC = NT == 2 ? 2 : 1;  // raw sources per stage
+  static constexpr int NSRC = NT == 2 ? 2 : (NT == 4 ? 3 : 1);  // raw sources per stage
+  template <int NT>
+  static constexpr int NRING = NT == 4 ? 4 : 2;  // ring layers
   template <int NT>
   static constexpr int TGT = NTGT<NT> * F * TXC;
   // Raw stages (RST) and target stages (TST): the TMA box of a source layer
@@ -94,17 +98,18 @@ struct Cfg {
   template <int NT>
   static constexpr int TST = MM == 1 ? HLF_M1_TST : (MM == 2 ? HLF_M2_TST : 1);
   template <int NT>
-  static constexpr int SMEM_DOUBLES = NSRC<NT> * RST<NT> * RAWS + 2 * RING + TST<NT> * TGT<NT>;
+  static constexpr int SMEM_DOUBLES = NSRC<NT> * RST<NT> * RAWS + NRING<NT> * RING + TST<NT> * TGT<NT>;
 };
 
 struct TParams {
-  CUtensorMap tmap[2];             // raw source tensors [layer][coef][y][x] for TMA box loads
+  CUtensorMap tmap[3];             // raw source tensors [layer][coef][y][x] for TMA box loads
   CUtensorMap tmapT[3];            // target tensors, box (32 cells, 1 row, F, 1 layer)
   double ML[kMaxN * (kMaxM + 1)];  // s! * M[s][l], l < m+1 (left block), row-major [s][l]
   double GM[kMaxB];                // G_k * k!/b!, indexed by bindex(b)
   double IF[kMaxM + 1];            // 1/o!
   const double* src;               // source field base (layer 0 of the allocation)
-  const double* src2;              // NT == 2: the V_y source
+  const double* src2;              // NT == 2, 4: the V_y source
+  const double* src3;              // NT == 4: the V_z source
   double* dst[3];                  // target field bases, per target component
   int64_t s_layer, s_plane;        // source strides
   int64_t t_layer, t_plane;        // target strides
@@ -323,7 +328,8 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
   constexpr int TST = G::template TST<NT>;   // target stages
   constexpr int NSRC = G::template NSRC<NT>;
   static_assert(RST >= 1 && RST <= 4 && TST >= 1 && TST <= 4, "stage counts");
-  constexpr bool MX = NT == 2;                // merged V_x + V_y pressure launch
+  constexpr bool MX = NT == 2 || NT == 4;     // merged V_x + V_y pressure launch (NT = 4: and V_z)
+  constexpr bool ALL3 = NT == 4;
   constexpr int NTT = G::template NTGT<NT>;   // target fields
   extern __shared__ __align__(128) double smem_raw[];
   // TMA tensor destinations must be 128 B aligned: align the base explicitly
@@ -336,7 +342,8 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
   double* rawbuf = smem + P.pre;
   double* ring0 = smem + NSRC * RST * G::RAWS;
   double* ring1 = ring0 + G::RING;
-  double* tgs = ring1 + G::RING;              // target stages [stage][t][f][cell] (lane-private path: stage 0)
+  double* tgs = ring0 + G::template NRING<NT> * G::RING;  // target stages [stage][t][f][cell] (lane-private path: stage 0)
+  // NT = 4: the V_z ring (layers ring1 + RING, + 2 RING)
   double* raw = rawbuf;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -434,11 +441,11 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
       const int stage = layer % RST;
       if (patch && tid < NSRC * ROWS) {
         const int si = tid / ROWS, r = tid - si * ROWS;
-        const double* base = (si ? P.src2 : P.src) + static_cast<int64_t>(layer) * P.s_layer;
+        const double* base = (si == 0 ? P.src : si == 1 ? P.src2 : P.src3) + static_cast<int64_t>(layer) * P.s_layer;
         pv = __ldg(base + static_cast<int64_t>(r >> 1) * P.s_plane + ((r & 1) ? yo1 : yo0) + xo_psx);
       }
       if (tid == 0) {
-        constexpr int NS = MX ? 2 : 1;
+        constexpr int NS = NSRC;
         mbar_expect_tx(&rawbar[stage], NSRC * G::RAW * 8);
         fence_proxy_async();
 #pragma unroll
@@ -450,9 +457,9 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
       return;
     }
 #pragma unroll
-   for (int si = 0; si < (MX ? 2 : 1); ++si) {
+   for (int si = 0; si < NSRC; ++si) {
     double* raw = rawbuf + ((layer % RST) * NSRC + si) * G::RAWS;
-    const double* base = (si ? P.src2 : P.src) + static_cast<int64_t>(layer) * P.s_layer;
+    const double* base = (si == 0 ? P.src : si == 1 ? P.src2 : P.src3) + static_cast<int64_t>(layer) * P.s_layer;
     if constexpr (ROWS % NWARP == 0) {
       // row r = warp + 8 i: coefficient plane (warp >> 1) + 4 i, source row warp & 1
       const double* q = base + static_cast<int64_t>(warp >> 1) * P.s_plane + ((warp & 1) ? yo1 : yo0) + xo_lane;
@@ -496,6 +503,7 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
     if constexpr (MX) {
       fix_walls_buf(st0, 0);
       fix_walls_buf(st0 + G::RAWS, 1);
+      if constexpr (ALL3) fix_walls_buf(st0 + 2 * G::RAWS, 2);
     } else {
       fix_walls_buf(st0, P.comp);
     }
@@ -612,6 +620,8 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
     for (int l = k0; l < k0 + TST - 1 && l < k1; ++l) issue_tgt(l);
   double* ro = ring1;
   double* rn = ring0;
+  double* roz = ring1 + 2 * G::RING;  // NT = 4 only
+  double* rnz = ring0 + 2 * G::RING;
   int emax = 0;  // max |high word| of the written values (finite check)
 #pragma unroll 1
   for (int k = k0 - 1; k < k1; ++k) {
@@ -624,7 +634,20 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
       issue_tgt(k + TST - 1);
     }
 #ifndef HLF_EXP_NOXY
-    if (MX && warp >= 2 * n1) {
+    if constexpr (ALL3) {
+      // tasks 0 .. 2 n1 - 1: merged V_x + V_y (l_z, q_x parity) into the
+      // ring; 2 n1 .. 4 n1 - 1: V_z (plain rows) into the V_z ring
+#pragma unroll 1
+      for (int task = warp; task < 4 * n1; task += NWARP) {
+        if (task < 2 * n1) {
+          const int lz = task >> 1;
+          const double* rbx = raw + lz * 2 * RAWX + lane;
+          xy_merged<MM>(task & 1, P, rbx, rbx + G::RAWS, rn + lz * TXC + lane);
+        } else {
+          xy_task<MM>(P, task - 2 * n1, raw + 2 * G::RAWS, rnz, lane);
+        }
+      }
+    } else if (MX && warp >= 2 * n1) {
       // m < 3: fewer (l_z, q_x parity) tasks than warps
     } else if constexpr (MX) {
       const int lz = warp >> 1;
@@ -659,6 +682,27 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
       double pt[nh][nh][nh];
       if constexpr (V7 && !V7S) v7_m3_z(ro + cbase, rn + cbase, cz, zg, pt);
       else if constexpr (!V7) z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
+      if constexpr (ALL3) {
+        // + the V_z term: its divergence reads P~_z[q + e_z], i.e. the other
+        // q_z class of the V_z ring, one class index up when PZ = 1 (warp-uniform)
+        double pz[nh][nh][nh];
+        z_stage<MM>(P, 1 - PZ, roz + cbase, rnz + cbase, pz);
+        if (PZ) {
+#pragma unroll
+          for (int a = 0; a < nh; ++a)
+#pragma unroll
+            for (int b = 0; b < nh; ++b)
+#pragma unroll
+              for (int d = 0; d + 1 < nh; ++d) pt[a][b][d] += pz[a][b][d + 1];
+        } else {
+#pragma unroll
+          for (int a = 0; a < nh; ++a)
+#pragma unroll
+            for (int b = 0; b < nh; ++b)
+#pragma unroll
+              for (int d = 0; d < nh; ++d) pt[a][b][d] += pz[a][b][d];
+        }
+      }
       const int64_t obase = static_cast<int64_t>(P.t_zoff + k) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
       if (P.tma_t) {
         const int ts = k % TST;
@@ -761,6 +805,11 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
     double* tmp = ro;
     ro = rn;
     rn = tmp;
+    if constexpr (ALL3) {
+      tmp = roz;
+      roz = rnz;
+      rnz = tmp;
+    }
   }
   if (emax >= 0x7ff00000 && zactive && P.step >= 0) report_nonfinite(P.flag, P.step);
 }
@@ -830,7 +879,8 @@ int launch_one(TParams T, cudaStream_t st) {
   if (T.tma) {
     const int layers = T.tNz + 3;
     T.tma = encode_raw_map<MM>(&T.tmap[0], T.src, T, layers) &&
-            (NT != 2 || encode_raw_map<MM>(&T.tmap[1], T.src2, T, layers));
+            (NT != 2 && NT != 4 || encode_raw_map<MM>(&T.tmap[1], T.src2, T, layers)) &&
+            (NT != 4 || encode_raw_map<MM>(&T.tmap[2], T.src3, T, layers));
   }
   using G = Cfg<MM>;
   const size_t smem = sizeof(double) * G::template SMEM_DOUBLES<NT> + 128;
@@ -892,9 +942,21 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.dst[0] = p.dst[0];
   int launched = 0;
   static const bool merge = std::getenv("HLF_NO_MERGE") == nullptr;
+  static const bool all3 = std::getenv("HLF_NO_ALL3") == nullptr;
   {
     // merged V_x + V_y launch: m = 3 +5.9 %, m = 1 +19.5 %, m = 2 +20 % (the
     // p read-modify-write of one pressure launch saved)
+    if constexpr (MM == 1) {
+      if (merge && all3) {
+        // m = 1: the whole pressure half step in one launch (three raw
+        // sources, the V_z term through a second ring)
+        T.comp = -1;
+        T.src = p.src[0];
+        T.src2 = p.src[1];
+        T.src3 = p.src[2];
+        return launch_one<MM, 4>(T, st);
+      }
+    }
     if (merge) {
       // V_x and V_y divergence terms in one launch, V_z in a second
       T.comp = -1;
