@@ -331,6 +331,11 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
   constexpr bool MX = NT == 2 || NT == 4;     // merged V_x + V_y pressure launch (NT = 4: and V_z)
   constexpr bool ALL3 = NT == 4;
   constexpr int NTT = G::template NTGT<NT>;   // target fields
+#ifndef HLF_XY_XFIRST
+  constexpr bool YF = MM == 3 && !ALL3;       // y-first XY stage (tiled3d_gen.cuh m3_yl / m3_xt)
+#else
+  constexpr bool YF = false;
+#endif
   extern __shared__ __align__(128) double smem_raw[];
   // TMA tensor destinations must be 128 B aligned: align the base explicitly
   // (the launch requests 128 B of slack)
@@ -634,7 +639,33 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
       issue_tgt(k + TST - 1);
     }
 #ifndef HLF_EXP_NOXY
-    if constexpr (ALL3) {
+    if constexpr (YF) {
+      // y-first XY (m = 3): warps (q_z, w2) sweep y in place over the raw
+      // stage (node = lane, q_x = 2 w2 + i; node 32 on lanes 0, 1), then the
+      // warp pair of q_z syncs and each warp sweeps x for j_y = w2 mod 2
+      const int qz = warp >> 1, w2 = warp & 1;
+#pragma unroll
+      for (int si = 0; si < NSRC; ++si) {
+        double* sb = raw + si * G::RAWS + qz * 2 * RAWX;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          double* yb = sb + (2 * w2 + i) * n1 * n1 * 2 * RAWX + lane;
+          if (MX && si == 1) m3_yl_sh(P, yb); else m3_yl(P, yb);
+        }
+        if (lane < 2) {
+          double* yb = sb + (2 * w2 + lane) * n1 * n1 * 2 * RAWX + TXC;
+          if (MX && si == 1) m3_yl_sh(P, yb); else m3_yl(P, yb);
+        }
+      }
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + qz) : "memory");
+      const double* xb = raw + qz * 2 * RAWX + lane;
+      double* wb = rn + qz * TXC + lane;
+      if constexpr (MX) {
+        if (w2) m3_xt1_vxy(P, xb, xb + G::RAWS, wb); else m3_xt0_vxy(P, xb, xb + G::RAWS, wb);
+      } else {
+        if (w2) m3_xt1(P, xb, wb); else m3_xt0(P, xb, wb);
+      }
+    } else if constexpr (ALL3) {
       // tasks 0 .. 2 n1 - 1: merged V_x + V_y (l_z, q_x parity) into the
       // ring; 2 n1 .. 4 n1 - 1: V_z (plain rows) into the V_z ring
 #pragma unroll 1

@@ -226,6 +226,66 @@ def gen_vel_q_shared(mm):
     return "\n".join(L)
 
 
+# ---------------------------------------------------------------- y-first XY
+# m = 3: the y sweep runs first, once per source node and (q_x, q_z) pair (the
+# two source rows of a cell row belong to that row alone, so no line is swept
+# twice), in place over the raw stage; the x sweep then runs on the y results
+# of neighbouring nodes.  x-first sweeps every source row for both cell rows
+# that share it (2 (m+1)^2 x-lines per cell instead of (m+1)^2).
+#   raw / Y index: (((qx*n1 + qy)*n1 + qz)*2 + sy)*RAWX + node; the y line of
+#   (qx, qz) at a node reads slots (qy, sy) and writes output jy to slot
+#   (qy, sy) = (jy >> 1, jy & 1).
+def yslot(mm, qx, jy, qz):
+    n1 = mm + 1
+    return (((qx * n1 + (jy >> 1)) * n1 + qz) * 2 + (jy & 1)) * RAWX
+
+
+def gen_yline(mm, shy, suffix):
+    n1, n = mm + 1, 2 * mm + 2
+    L = [f"__device__ __forceinline__ void m{mm}_yl{suffix}(const TParams& P, double* __restrict__ yb) {{",
+         "  // yb = raw + (qx*n1*n1 + qz)*2*RAWX + node: one y line, in place"]
+    src = {}
+    for sy in range(2):
+        for l in range(n1):
+            nm = f"r{sy}{l}"
+            L.append(f"  const double {nm} = yb[{(l * n1 * 2 + sy) * RAWX}];")
+            src[(sy, l)] = nm
+    res = half_line(mm, lambda l: src[(0, l)], lambda l: src[(1, l)], list(range(n)), "y", L, shy)
+    for jy in range(n):
+        L.append(f"  yb[{((jy >> 1) * n1 * 2 + (jy & 1)) * RAWX}] = {res[jy]};")
+    L.append("}")
+    return "\n".join(L)
+
+
+def gen_xtask(mm, jyp, merged):
+    """x lines of one (q_z, j_y parity) task: jy = jyp, jyp+2, ...; full lines
+    (all n outputs j_x) into the ring.  merged: V_x through rows q_x+1 plus V_y."""
+    n1, n = mm + 1, 2 * mm + 2
+    if merged:
+        L = [f"__device__ __forceinline__ void m{mm}_xt{jyp}_vxy(const TParams& P, const double* __restrict__ xbx,",
+             "    const double* __restrict__ xby, double* __restrict__ wb) {"]
+        flds = (("a", "xbx", 1), ("b", "xby", 0))
+    else:
+        L = [f"__device__ __forceinline__ void m{mm}_xt{jyp}(const TParams& P, const double* __restrict__ xbx,",
+             "    double* __restrict__ wb) {"]
+        flds = (("a", "xbx", 0),)
+    L.append("  // xb = Y + qz*2*RAWX + lane;  wb = ring_new + qz*TXC + lane")
+    for jy in range(jyp, n, 2):
+        outs = {}
+        for fld, xb, shx in flds:
+            def off(l, side, jy=jy, xb=xb):
+                return f"{xb}[{yslot(mm, l, jy, 0) + side}]"
+            res = half_line(mm, lambda l: off(l, 0), lambda l: off(l, 1), list(range(n)), f"{fld}{jy}", L, shx)
+            for jx, nm in res.items():
+                if nm != "0.0":
+                    outs.setdefault(jx, []).append(nm)
+        for jx in range(n):
+            terms = outs.get(jx, [])
+            L.append(f"  wb[{(jx * n + jy) * n1 * TXC}] = {' + '.join(terms) if terms else '0.0'};")
+    L.append("}")
+    return "\n".join(L)
+
+
 def main():
     parts = ["// GENERATED by tools/gen_tiled3d.py -- do not edit.",
              "// Stage code of the tiled 3D Hermite-leapfrog kernel (kernels_tiled3d.cu).",
@@ -305,6 +365,16 @@ def main():
         if mm == 3:
             parts.append(gen_vel_q_shared(mm))
             parts.append("")
+            # y-first XY stage (kernels_tiled3d.cu, m = 3)
+            parts.append(gen_yline(mm, 0, ""))
+            parts.append("")
+            parts.append(gen_yline(mm, 1, "_sh"))
+            parts.append("")
+            for jyp in range(2):
+                parts.append(gen_xtask(mm, jyp, False))
+                parts.append("")
+                parts.append(gen_xtask(mm, jyp, True))
+                parts.append("")
         parts.append(f"// m = {mm}: {len(bodies)} distinct CK bodies")
         parts.append("")
     with open(OUT, "w") as f:
