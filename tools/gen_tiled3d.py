@@ -42,6 +42,14 @@ def bindex(b, mm):
     raise ValueError(b)
 
 
+def mzero(r, l, mm):
+    """M[r][l] is exactly zero for even rows r >= 2 and l = 0 (the value
+    coefficient of the even Taylor orders); the host checks it for the fast
+    kernels (hlf_capi.cu, m_mirror) and these terms are not emitted.  From m = 4
+    on the reference's LU inverse leaves round-off there, which is kept."""
+    return mm <= 3 and l == 0 and r >= 2 and r % 2 == 0
+
+
 def half_line(mm, srcL, srcR, outs, tmp, lines, sh=0):
     """outputs s in `outs` of a parity-split line from L/R expressions.  sh = 1
     uses row s+1 of M for output s (the index shift of a divergence term,
@@ -52,7 +60,8 @@ def half_line(mm, srcL, srcR, outs, tmp, lines, sh=0):
         if s + sh >= n:
             continue
         for l in range(n1):
-            (need_s if (s + sh + l) % 2 == 0 else need_d).add(l)
+            if not mzero(s + sh, l, mm):
+                (need_s if (s + sh + l) % 2 == 0 else need_d).add(l)
     for l in sorted(need_s):
         lines.append(f"  const double {tmp}s{l} = {srcL(l)} + {srcR(l)};")
     for l in sorted(need_d):
@@ -65,6 +74,8 @@ def half_line(mm, srcL, srcR, outs, tmp, lines, sh=0):
             continue
         expr = "0.0"
         for l in range(n1):
+            if mzero(r, l, mm):
+                continue
             if (r + l) % 2 == 0:
                 expr = f"fma(P.ML[{r * n1 + l}], {tmp}s{l}, {expr})"
             else:
