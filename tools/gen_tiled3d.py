@@ -282,17 +282,35 @@ def gen_xtask(mm, jyp, merged):
         flds = (("a", "xbx", 0),)
     L.append("  // xb = Y + qz*2*RAWX + lane;  wb = ring_new + qz*TXC + lane")
     for jy in range(jyp, n, 2):
-        outs = {}
+        # one FMA chain per output over both fields' sum / difference terms
+        # (the merged launch: no separate add of the two lines)
+        chains = {jx: "0.0" for jx in range(n)}
         for fld, xb, shx in flds:
             def off(l, side, jy=jy, xb=xb):
                 return f"{xb}[{yslot(mm, l, jy, 0) + side}]"
-            res = half_line(mm, lambda l: off(l, 0), lambda l: off(l, 1), list(range(n)), f"{fld}{jy}", L, shx)
-            for jx, nm in res.items():
-                if nm != "0.0":
-                    outs.setdefault(jx, []).append(nm)
+            need_s, need_d = set(), set()
+            for jx in range(n):
+                r = jx + shx
+                for l in range(n1):
+                    if r < n and not mzero(r, l, mm):
+                        (need_s if (r + l) % 2 == 0 else need_d).add(l)
+            for l in sorted(need_s):
+                L.append(f"  const double {fld}{jy}s{l} = {off(l, 0)} + {off(l, 1)};")
+            for l in sorted(need_d):
+                L.append(f"  const double {fld}{jy}d{l} = {off(l, 1)} - {off(l, 0)};")
+            for jx in range(n):
+                r = jx + shx
+                if r >= n:
+                    continue
+                for l in range(n1):
+                    if mzero(r, l, mm):
+                        continue
+                    if (r + l) % 2 == 0:
+                        chains[jx] = f"fma(P.ML[{r * n1 + l}], {fld}{jy}s{l}, {chains[jx]})"
+                    else:
+                        chains[jx] = f"fma(-P.ML[{r * n1 + l}], {fld}{jy}d{l}, {chains[jx]})"
         for jx in range(n):
-            terms = outs.get(jx, [])
-            L.append(f"  wb[{(jx * n + jy) * n1 * TXC}] = {' + '.join(terms) if terms else '0.0'};")
+            L.append(f"  wb[{(jx * n + jy) * n1 * TXC}] = {chains[jx]};")
     L.append("}")
     return "\n".join(L)
 
