@@ -9,6 +9,9 @@
 //          source rows (reconstruct_cell_2d's first sweep, interpolation.cpp:87-99);
 //   (Y)    applies M along y: n (m+1) y-lines per cell (interpolation.cpp:101-112);
 //          the result for source layer k+1 goes into a 2-layer ring;
+//          m = 3 sweeps y first instead, once per source node, in place over
+//          the raw stage, then x on neighbouring nodes ((m+1)^2 + n (m+1)
+//          lines per cell instead of 2 (m+1)^2 + n (m+1));
 //   (Z+CK) applies M along z between ring layers k and k+1 and immediately
 //          contracts with the closed-form odd Cauchy-Kowalewski sum of the
 //          leapfrog half update (stepper1d.cpp:22-61).
