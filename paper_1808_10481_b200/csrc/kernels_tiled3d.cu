@@ -57,6 +57,7 @@ constexpr int NTHREADS = NWARP * 32;
 #endif
 constexpr int ZC = HLF_ZC;      // target layers per CTA (with TMA loads: 64 +0.9 % over 128, 256 -1.5 %)
 constexpr int kMaxB = 20;       // multi-indices |b| <= 3
+constexpr int kRZ = 2 * 10 * 2 * 4;  // z-folded CK rows: [PZo][(a, b), a + b <= 3][jzo][l] (m = 3)
 
 template <int MM>
 struct Cfg {
@@ -110,6 +111,7 @@ struct TParams {
   double ML[kMaxN * (kMaxM + 1)];  // s! * M[s][l], l < m+1 (left block), row-major [s][l]
   double GM[kMaxB];                // G_k * k!/b!, indexed by bindex(b)
   double IF[kMaxM + 1];            // 1/o!
+  double RZ[kRZ];                  // pressure launches, m = 3: z sweep folded into the CK (rz_table)
   const double* src;               // source field base (layer 0 of the allocation)
   const double* src2;              // NT == 2, 4: the V_y source
   const double* src3;              // NT == 4: the V_z source
@@ -540,12 +542,22 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
   // but the velocity launch, with three CK bodies and the z-shift selects of
   // its z component, is faster in the plain one-class-per-warp layout
   // (62.2 vs 68.8 ms at 512x512x256).  HLF_NO_V7 / HLF_V7 force one layout.
+  // ZF (m = 3 pressure launches): the z sweep folded into the CK
+  // (tiled3d_gen.cuh m3_zf_*: 4 FMAs per (ring column, output) from the
+  // column's sum / difference values and the host rows RZ, instead of the z
+  // half line plus the CK terms; one output class per warp, the plain
+  // layout, warp-uniform rows as constant operands).  HLF_NO_ZF: V7 below.
+#if defined(HLF_NO_ZF)
+  constexpr bool ZF = false;
+#else
+  constexpr bool ZF = MM == 3 && (NT == 1 || NT == 2);
+#endif
 #if defined(HLF_NO_V7)
   constexpr bool V7 = false;
 #elif defined(HLF_V7)
-  constexpr bool V7 = MM == 3;
+  constexpr bool V7 = MM == 3 && !ZF;
 #else
-  constexpr bool V7 = MM == 3 && NT != 3;
+  constexpr bool V7 = MM == 3 && NT != 3 && !ZF;
 #endif
   // V7S: the V7 Z stage and CK fused per class column (streaming; one column
   // of P~ live instead of 64).  HLF_V7_SPLIT keeps the two stages apart.
@@ -586,7 +598,7 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
       const int64_t ob = static_cast<int64_t>(P.t_zoff + kk) * P.t_layer + static_cast<int64_t>(ty) * P.tNx + x0 + zcell;
 #pragma unroll 1
       for (int t = 0; t < NTT; ++t) {
-        const int c = MX ? -1 : (NT == 3 ? t : P.comp);
+        const int c = MX || ZF ? -1 : (NT == 3 ? t : P.comp);  // ZF: class = output parity
         const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
         const int f0 = (sx * n1 + sy) * n1 + sz;
         const double* q = P.dst[t] + ob + f0 * P.t_plane32;
@@ -714,8 +726,13 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
 #endif
       // Z stage + CK for this warp's parity class
       double pt[nh][nh][nh];
+      // ZF runs the merged launch and the V_z launch (the only pressure
+      // launches at m = 3 unless HLF_NO_ZF: launch_m ignores HLF_NO_MERGE)
+      constexpr bool zf = ZF;
       if constexpr (V7 && !V7S) v7_m3_z(ro + cbase, rn + cbase, cz, zg, pt);
-      else if constexpr (!V7) z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
+      else if constexpr (!V7) {
+        if (!zf) z_stage<MM>(P, PZ, ro + cbase, rn + cbase, pt);
+      }
       if constexpr (ALL3) {
         // + the V_z term: its divergence reads P~_z[q + e_z], i.e. the other
         // q_z class of the V_z ring, one class index up when PZ = 1 (warp-uniform)
@@ -780,6 +797,7 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
 #pragma unroll
       for (int t = 0; t < NTT; ++t) {
         const int c = MX ? -1 : (NT == 3 ? t : P.comp);  // -1: shifts already in the XY rows
+        const int ce = zf ? -1 : c;  // ZF: the warp's class is the output parity
         double acc[jh][jh][jh];
 #pragma unroll
         for (int a = 0; a < jh; ++a)
@@ -789,7 +807,7 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
             for (int d = 0; d < jh; ++d) acc[a][b][d] = 0.0;
         // outputs o = s + 2j (s = the class's output parity for component c):
         // one base address per component, compile-time offsets per j
-        const int sx = (PX - (c == 0)) & 1, sy = (PY - (c == 1)) & 1, sz = (PZ - (c == 2)) & 1;
+        const int sx = (PX - (ce == 0)) & 1, sy = (PY - (ce == 1)) & 1, sz = (PZ - (ce == 2)) & 1;
         const int f0 = (sx * n1 + sy) * n1 + sz;
         double* dp = P.dst[t] + obase + f0 * P.t_plane32;
         asm("" : "+l"(dp));  // keep dp a base register: one IMAD.WIDE per output address
@@ -805,7 +823,17 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
               for (int d = 0; d < jh; ++d) acc[a][b][d] = accq[VQ ? t : 0][a][b][d];
         } else if constexpr (V7S) v7_zck(c, PX, PY, PZ, P, ro + cbase, rn + cbase, cz, zg, acc);
         else if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);
-        else ck_any<MM>(c, warp, P, pt, acc);
+        else if (zf) {
+          if constexpr (ZF) {
+            const double* a0 = ro + cbase;
+            const double* a1 = rn + cbase;
+            if (MX) {
+              if (PZ) m3_zf_s0_pz1(P, a0, a1, acc); else m3_zf_s0_pz0(P, a0, a1, acc);
+            } else {
+              if (PZ) m3_zf_s1_pz1(P, a0, a1, acc); else m3_zf_s1_pz0(P, a0, a1, acc);
+            }
+          }
+        } else ck_any<MM>(c, warp, P, pt, acc);
 #else
         acc[0][0][0] += pt[0][0][0] + pt[3][3][3] + pt[1][2][3];
 #endif
@@ -942,6 +970,29 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
         T.GM[bindex(b0, b1, b2, MM)] = p.G[k] * host_fact(k) / (host_fact(b0) * host_fact(b1) * host_fact(b2));
       }
   for (int o = 0; o <= MM; ++o) T.IF[o] = 1.0 / host_fact(o);
+  auto rz_table = [&](int sh) {
+    // RZ[PZo][(a, b)][jzo][l] = sum_c GM[a, b, c] (+-) s! M[s][l], s = oz + 2c + sh
+    // (oz = PZo + 2 jzo; + for s + l even (sum), - for odd (difference));
+    // tools/gen_tiled3d.py gen_zf
+    if constexpr (MM == 3) {
+      int ab = 0;
+      for (int a = 0; a <= MM; ++a)
+        for (int b = 0; b <= MM - a; ++b, ++ab)
+          for (int pzo = 0; pzo < 2; ++pzo)
+            for (int jzo = 0; jzo < 2; ++jzo)
+              for (int l = 0; l < n1; ++l) {
+                double r = 0.0;
+                const int oz = pzo + 2 * jzo;
+                for (int c = 0; a + b + c <= MM; ++c) {
+                  const int s = oz + 2 * c + sh;
+                  if (s >= n) break;
+                  r += T.GM[bindex(a, b, c, MM)] * (((s + l) & 1) ? -T.ML[s * n1 + l] : T.ML[s * n1 + l]);
+                }
+                T.RZ[((pzo * 10 + ab) * 2 + jzo) * n1 + l] = r;
+              }
+    }
+    (void)sh;
+  };
   T.s_layer = p.s_layer;
   T.s_plane = p.s_coef;
   T.t_layer = p.t_layer;
@@ -975,7 +1026,15 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.pre = 1;
   T.dst[0] = p.dst[0];
   int launched = 0;
+  // m = 3 with the z-folded CK has no single V_x / V_y pressure launches
+  // (m = 3 with the z-folded CK has no single V_x / V_y pressure launches:
+  // HLF_NO_MERGE applies to m < 3 and to HLF_NO_ZF builds)
   static const bool merge = std::getenv("HLF_NO_MERGE") == nullptr;
+#ifdef HLF_NO_ZF
+  constexpr bool force_merge = false;
+#else
+  constexpr bool force_merge = MM == 3;
+#endif
   static const bool all3 = std::getenv("HLF_NO_ALL3") == nullptr;
   {
     // merged V_x + V_y launch: m = 3 +5.9 %, m = 1 +19.5 %, m = 2 +20 % (the
@@ -991,20 +1050,23 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
         return launch_one<MM, 4>(T, st);
       }
     }
-    if (merge) {
+    if (merge || force_merge) {
       // V_x and V_y divergence terms in one launch, V_z in a second
       T.comp = -1;
       T.src = p.src[0];
       T.src2 = p.src[1];
+      rz_table(0);
       launched += launch_one<MM, 2>(T, st);
       T.comp = 2;
       T.src = p.src[2];
+      rz_table(1);
       return launched + launch_one<MM, 1>(T, st);
     }
   }
   for (int c = 0; c < 3; ++c) {
     T.comp = c;
     T.src = p.src[c];
+    if (c == 2) rz_table(1);
     launched += launch_one<MM, 1>(T, st);
   }
   return launched;

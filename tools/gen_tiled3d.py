@@ -315,6 +315,79 @@ def gen_xtask(mm, jyp, merged):
     return "\n".join(L)
 
 
+# ---------------------------------------------------------------- z-folded CK
+# Pressure launches, m = 3: the z sweep is folded into the CK.  For output
+# o = (ox, oy, oz) of class parity (PX, PY, PZo) and a ring column (jx, jy) =
+# (ox + 2a, oy + 2b) (class-local ix = jxo + a, iy = jyo + b):
+#   sum_c GM[a,b,c] P~[jx, jy, oz + 2c + sh] = sum_l R[a,b][jzo][l] w_l,
+#   R[a,b][jzo][l] = sum_c GM[a,b,c] (+-) s! M[s][l],  s = oz + 2c + sh < n,
+# w_l = sigma_l (s + l even) or delta_l (odd) of the column's two ring layers
+# (sh = 1: the V_z divergence term's index shift).  4 FMAs per (column,
+# output) instead of the z half line (16) plus the CK terms that read it.
+# The host fills R (TParams.RZ[PZo][ab][jzo][l], kernels_tiled3d.cu rz_table).
+def ab_index(a, b, mm):
+    idx = 0
+    for a0 in range(mm + 1):
+        for b0 in range(mm + 1 - a0):
+            if (a0, b0) == (a, b):
+                return idx
+            idx += 1
+    raise ValueError((a, b))
+
+
+def rz_zero(mm, sh, pzo, jzo, l):
+    """R[..][jzo][l] is exactly zero when every row s it sums has M[s][l] = 0"""
+    n = 2 * mm + 2
+    oz = pzo + 2 * jzo
+    rows = [oz + 2 * c + sh for c in range(mm + 1) if oz + 2 * c + sh < n]
+    return all(mzero(r, l, mm) for r in rows)
+
+
+def gen_zf(mm, pzo, sh):
+    n1, n = mm + 1, 2 * mm + 2
+    nh, jh = n // 2, (n1 + 1) // 2
+    nab = (mm + 1) * (mm + 2) // 2
+    L = [f"__device__ __forceinline__ void m{mm}_zf_s{sh}_pz{pzo}(const TParams& P, const double* __restrict__ ro,",
+         f"    const double* __restrict__ rn, double (&acc)[{jh}][{jh}][{jh}]) {{",
+         "  // ro/rn = ring + ((PX*n + PY)*n1)*TXC + lane (non-V7 layout); class = output parity"]
+    for ix in range(nh):
+        for iy in range(nh):
+            terms = []
+            for jxo in range(jh):
+                for jyo in range(jh):
+                    a, b = ix - jxo, iy - jyo
+                    if a < 0 or b < 0 or a + b > mm:
+                        continue
+                    for jzo in range(jh):
+                        terms.append((jxo, jyo, jzo, ab_index(a, b, mm)))
+            if not terms:
+                continue
+            off = ((2 * ix) * n + 2 * iy) * n1 * TXC
+            L.append("  {")
+            # sigma / delta the terms need: w_l = sigma_l if (oz + sh + l) even
+            need = set()
+            for (_, _, jzo, _) in terms:
+                for l in range(n1):
+                    if not rz_zero(mm, sh, pzo, jzo, l):
+                        need.add(l)
+            for l in sorted(need):
+                if (pzo + sh + l) % 2 == 0:
+                    L.append(f"    const double w{l} = ro[{off + l * TXC}] + rn[{off + l * TXC}];")
+                else:
+                    L.append(f"    const double w{l} = rn[{off + l * TXC}] - ro[{off + l * TXC}];")
+            for (jxo, jyo, jzo, ab) in terms:
+                nm = f"acc[{jxo}][{jyo}][{jzo}]"
+                expr = nm
+                for l in range(n1):
+                    if rz_zero(mm, sh, pzo, jzo, l):
+                        continue
+                    expr = f"fma(P.RZ[{((pzo * nab + ab) * jh + jzo) * n1 + l}], w{l}, {expr})"
+                L.append(f"    {nm} = {expr};")
+            L.append("  }")
+    L.append("}")
+    return "\n".join(L)
+
+
 def main():
     parts = ["// GENERATED by tools/gen_tiled3d.py -- do not edit.",
              "// Stage code of the tiled 3D Hermite-leapfrog kernel (kernels_tiled3d.cu).",
@@ -399,6 +472,10 @@ def main():
             parts.append("")
             parts.append(gen_yline(mm, 1, "_sh"))
             parts.append("")
+            for sh in range(2):
+                for pzo in range(2):
+                    parts.append(gen_zf(mm, pzo, sh))
+                    parts.append("")
             for jyp in range(2):
                 parts.append(gen_xtask(mm, jyp, False))
                 parts.append("")

@@ -18,6 +18,7 @@ import paper_1808_10481_b200 as H
 
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 K = tuple(int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "512x512x256").split("x"))
+KINDS = sys.argv[3].split(",") if len(sys.argv) > 3 else ["vel", "pre", "step"]
 
 
 class Smi:
@@ -51,10 +52,16 @@ for c in range(1, 4):
     g.fill_separable(c, -0.1, [pi] * 3, [pi / 2 if a == c - 1 else 0.0 for a in range(3)])
 dt = 0.9 * g.grid.h / math.sqrt(3)
 res = {"m": m, "K": K}
-for name in ("vel", "pre", "step"):
+for name in KINDS:
     # forward then backward in time keeps the data bounded (dt -> -dt)
     g.set_times(0, dt / 2, dt)
-    fn = {"vel": g.advance_v, "pre": g.advance_p, "step": lambda: g.step_system(0)}[name]
+    raw = {"vel": g.advance_v, "pre": g.advance_p, "step": lambda: g.step_system(0)}[name]
+
+    def fn(raw=raw):
+        try:  # ablation builds (HLF_EXP_*) produce garbage: time them anyway
+            raw()
+        except H.InstabilityError:
+            g.clear_finite()
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -75,5 +82,6 @@ for name in ("vel", "pre", "step"):
     res[name] = {"ms": round(ms, 3), "sm_mhz_median": statistics.median(float(r[0]) for r in load) if load else None,
                  "power_w_median": statistics.median(float(r[1]) for r in load) if load else None,
                  "power_cap_frac": round(sum(r[2] == "Active" for r in load) / max(1, len(load)), 2),
+                 "joules": round(ms * 1e-3 * statistics.median(float(r[1]) for r in load), 2) if load else None,
                  "samples": len(load)}
 print(json.dumps(res))
