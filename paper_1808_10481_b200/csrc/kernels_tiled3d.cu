@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
 #if defined(HLF_NO_ZF)
   constexpr bool ZF = false;
 #else
-  constexpr bool ZF = MM == 3 && (NT == 1 || NT == 2);
+  constexpr bool ZF = MM >= 2 && (NT == 1 || NT == 2);
 #endif
 #if defined(HLF_NO_V7)
   constexpr bool V7 = false;
@@ -824,13 +824,21 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
         } else if constexpr (V7S) v7_zck(c, PX, PY, PZ, P, ro + cbase, rn + cbase, cz, zg, acc);
         else if constexpr (V7) v7_ck(c, PX, PY, PZ, P, pt, acc);
         else if (zf) {
-          if constexpr (ZF) {
+          if constexpr (ZF && MM == 3) {
             const double* a0 = ro + cbase;
             const double* a1 = rn + cbase;
             if (MX) {
               if (PZ) m3_zf_s0_pz1(P, a0, a1, acc); else m3_zf_s0_pz0(P, a0, a1, acc);
             } else {
               if (PZ) m3_zf_s1_pz1(P, a0, a1, acc); else m3_zf_s1_pz0(P, a0, a1, acc);
+            }
+          } else if constexpr (ZF && MM == 2) {
+            const double* a0 = ro + cbase;
+            const double* a1 = rn + cbase;
+            if (MX) {
+              if (PZ) m2_zf_s0_pz1(P, a0, a1, acc); else m2_zf_s0_pz0(P, a0, a1, acc);
+            } else {
+              if (PZ) m2_zf_s1_pz1(P, a0, a1, acc); else m2_zf_s1_pz0(P, a0, a1, acc);
             }
           }
         } else ck_any<MM>(c, warp, P, pt, acc);
@@ -974,7 +982,8 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
     // RZ[PZo][(a, b)][jzo][l] = sum_c GM[a, b, c] (+-) s! M[s][l], s = oz + 2c + sh
     // (oz = PZo + 2 jzo; + for s + l even (sum), - for odd (difference));
     // tools/gen_tiled3d.py gen_zf
-    if constexpr (MM == 3) {
+    if constexpr (MM >= 2) {
+      constexpr int nab = (MM + 1) * (MM + 2) / 2, jhh = (n1 + 1) / 2;
       int ab = 0;
       for (int a = 0; a <= MM; ++a)
         for (int b = 0; b <= MM - a; ++b, ++ab)
@@ -988,7 +997,7 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
                   if (s >= n) break;
                   r += T.GM[bindex(a, b, c, MM)] * (((s + l) & 1) ? -T.ML[s * n1 + l] : T.ML[s * n1 + l]);
                 }
-                T.RZ[((pzo * 10 + ab) * 2 + jzo) * n1 + l] = r;
+                T.RZ[((pzo * nab + ab) * jhh + jzo) * n1 + l] = r;
               }
     }
     (void)sh;
@@ -1026,14 +1035,13 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   T.pre = 1;
   T.dst[0] = p.dst[0];
   int launched = 0;
-  // m = 3 with the z-folded CK has no single V_x / V_y pressure launches
-  // (m = 3 with the z-folded CK has no single V_x / V_y pressure launches:
-  // HLF_NO_MERGE applies to m < 3 and to HLF_NO_ZF builds)
+  // m = 2, 3 with the z-folded CK have no single V_x / V_y pressure launches
+  // (HLF_NO_MERGE applies to m = 1 and to HLF_NO_ZF builds)
   static const bool merge = std::getenv("HLF_NO_MERGE") == nullptr;
 #ifdef HLF_NO_ZF
   constexpr bool force_merge = false;
 #else
-  constexpr bool force_merge = MM == 3;
+  constexpr bool force_merge = MM >= 2;
 #endif
   static const bool all3 = std::getenv("HLF_NO_ALL3") == nullptr;
   {

@@ -359,7 +359,8 @@ def gen_zf(mm, pzo, sh):
                     if a < 0 or b < 0 or a + b > mm:
                         continue
                     for jzo in range(jh):
-                        terms.append((jxo, jyo, jzo, ab_index(a, b, mm)))
+                        if pzo + 2 * jzo <= mm:  # o_z <= m (m = 2: PZo = 1 has one output layer)
+                            terms.append((jxo, jyo, jzo, ab_index(a, b, mm)))
             if not terms:
                 continue
             off = ((2 * ix) * n + 2 * iy) * n1 * TXC
@@ -464,6 +465,12 @@ def main():
         parts.append("  }")
         parts.append("}")
         parts.append("")
+        if mm >= 2:
+            # z-folded CK of the pressure launches (m = 2, 3)
+            for sh in range(2):
+                for pzo in range(2):
+                    parts.append(gen_zf(mm, pzo, sh))
+                    parts.append("")
         if mm == 3:
             parts.append(gen_vel_q_shared(mm))
             parts.append("")
@@ -472,10 +479,7 @@ def main():
             parts.append("")
             parts.append(gen_yline(mm, 1, "_sh"))
             parts.append("")
-            for sh in range(2):
-                for pzo in range(2):
-                    parts.append(gen_zf(mm, pzo, sh))
-                    parts.append("")
+
             for jyp in range(2):
                 parts.append(gen_xtask(mm, jyp, False))
                 parts.append("")
