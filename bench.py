@@ -64,7 +64,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, index: int):
         self.index = index
@@ -78,7 +78,7 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 parts = [p.strip() for p in out.stdout.strip().split(",")]
-                if len(parts) == 6:
+                if len(parts) == 8:
                     self.samples.append(parts)
             except Exception:
                 pass
@@ -101,8 +101,18 @@ class ClockSampler:
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        pw = [x for x in (num(s[6]) for s in self.samples) if x is not None]
+        pl = [x for x in (num(s[7]) for s in self.samples) if x is not None]
+        # board power next to the clocks: the 3D m = 3 launches run at the
+        # power limit (profiles/r2b/launch_power.json)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_median": statistics.median(pw) if pw else None, "power_limit_w": max(pl) if pl else None}
 
 
 # Algorithmic work per cell of the three launches of one 3D m = 3 step
@@ -187,8 +197,7 @@ def roofline_block(kt, pk, cells, step_ms, dof_local):
         key = dom["kernel"].split("tiled3d<")[-1].split(">")[0]
         if key in per:
             top["traffic"] = per[key] * cells
-            top["traffic_src"] = (tr.get("source", "") + "; per-cell DRAM bytes x cells (the per-cell traffic does "
-                                  "not depend on nz: every CTA marches 64-layer z chunks either way)")
+            top["traffic_src"] = tr.get("source", "") + "; per-cell DRAM bytes x cells"
     except Exception:
         pass
     return top

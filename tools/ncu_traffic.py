@@ -1,8 +1,8 @@
-"""Write profiles/ncu_traffic.json from an `ncu --set full` report of
-`bench.py --steps 1 --warmup 3 --nz NZ --no-e2e --no-cpu-baseline` (the bench
-workload with NZ z layers instead of 256; identical CTA / tile / z-chunk
-structure): DRAM bytes per launch of the tiled3d kernels, per cell, scaled to
-the bench's 512 x 512 x 256 grid.  bench.py reads `pre_dram_bytes_per_launch`
+"""Write profiles/ncu_traffic.json from an ncu report (--set full, or just the
+dram__bytes_read/write metrics) of `bench.py --steps 1 --warmup 3 [--nz NZ]
+--no-e2e --no-cpu-baseline` (the bench workload, or the same CTA / tile /
+z-chunk structure with NZ z layers): DRAM bytes per launch of the tiled3d
+kernels, per cell, scaled to the bench's 512 x 512 x 256 grid.  bench.py reads `pre_dram_bytes_per_launch`
 for the roofline line's `traffic`.
 Usage: python tools/ncu_traffic.py REPORT.ncu-rep NZ"""
 import csv
