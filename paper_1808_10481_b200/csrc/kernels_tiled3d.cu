@@ -128,6 +128,7 @@ struct TParams {
   int step;
   int tma;                         // strides allow 16 B aligned TMA row copies
   int tma_t;                       // target tensor maps encoded
+  int raster;                      // > 0: CTA rows launched in groups of `raster` y rows (below)
   int* flag;
   unsigned long long* ctr;         // path counters of this half step (tests) or null
   const HalfParams* hp;            // host only: the caller's parameters (launch timing)
@@ -357,8 +358,19 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
   double* raw = rawbuf;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int x0 = blockIdx.x * TXC;
-  const int ty = blockIdx.y;
+  // CTA order: a source row is read by cell rows ty and ty + 1; launched
+  // x-fastest those two CTAs start gridDim.x apart and the second read misses
+  // L2 part of the time.  With raster = G the rows of an x tile go in groups
+  // of G consecutive CTAs (y fastest inside the group), x tiles next.
+  int bx = blockIdx.x, ty = blockIdx.y;
+  if (P.raster > 1) {
+    const int lin = blockIdx.x + gridDim.x * blockIdx.y;
+    const int grp = lin / (P.raster * gridDim.x), r = lin - grp * P.raster * gridDim.x;
+    const int rows = min(P.raster, static_cast<int>(gridDim.y) - grp * P.raster);
+    ty = grp * P.raster + r % rows;
+    bx = r / rows;
+  }
+  const int x0 = bx * TXC;
   const int k0 = blockIdx.z * ZC;
   const int k1 = min(k0 + ZC, P.tNz);
   if (k0 >= k1) return;
@@ -1025,6 +1037,12 @@ int launch_m(HalfKind kind, const HalfParams& p, cudaStream_t st) {
   // TMA boxes: 16 B aligned strides and bases (checked again per tensor map)
   T.tma = std::getenv("HLF_NO_TMA") == nullptr && p.s_layer % 2 == 0 && p.s_coef % 2 == 0 && p.sNx % 2 == 0;
   T.tma_t = std::getenv("HLF_NO_TMA_T") == nullptr;
+  {
+    // m = 3: groups of 8 rows (merged pressure launch DRAM 2438 -> 2267 B per
+    // cell, step -0.9 %; m = 1, 2 +-0: tools/raster_sweep.sh, raster_ab.sh)
+    const char* e = std::getenv("HLF_RASTER");
+    T.raster = e ? std::atoi(e) : (MM == 3 ? 8 : 0);
+  }
   if (kind == VEL) {
     T.pre = 0;
     T.comp = 0;
