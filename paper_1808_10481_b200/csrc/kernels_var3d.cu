@@ -24,10 +24,21 @@
 // and Lap = sum_c d_c d_c (the two derivatives of the recurrence; av is a
 // scalar).  Arithmetic is reordered against the oracle (FMA, separable
 // products), so parity is at the 1e-12 bar, not bit-identical.
+#include <type_traits>
+
 #include "hlf_internal.cuh"
 
 namespace hlfk {
 namespace {
+
+// compile-time loop: f(std::integral_constant<int, I>) for I = B .. E-1
+template <int B, int E, class Fn>
+__device__ __forceinline__ void static_for(Fn&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
 
 constexpr int WARPS = 4;
 
@@ -246,8 +257,12 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
       // sweeps A->Cb, Cb->A, A->Cb: the result sits in Cb
     };
 
-    // X <- ap (.) X in place: X = -c0 X - c1 S_x S_y S_z X, with the S passes through B
-    auto ap_times = [&](double* X) {
+    // X <- ap (.) X in place: X = -c0 X - c1 S_x S_y S_z X, with the S passes through B.
+    // Only the box q <= lim (every axis) is computed: the truncated product at
+    // q reads entries <= q, and the later levels and the target read no
+    // entry outside the box of their level (lim from level_lim below)
+    auto ap_times = [&](double* X, auto limc) {
+      constexpr int lim = decltype(limc)::value;
       // z pass X -> B, y pass in B, x pass B -> X fused with -c0 X - c1 (.)
 #pragma unroll
       for (int ax = 2; ax >= 0; --ax) {
@@ -257,13 +272,15 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
         for (int it = 0; it < (n * n + 31) / 32; ++it) {
           const int l = lane + 32 * it;
           if (l >= n * n) break;
+          if (l / n > lim || l % n > lim) continue;  // the line's fixed coordinates
           int base, st;
           line_of<MM>(ax, l, base, st);
           double v[n];
 #pragma unroll
-          for (int i = 0; i < n; ++i) v[i] = in[base + i * st];
+          for (int i = 0; i < n; ++i) v[i] = i <= lim ? in[base + i * st] : 0.0;
 #pragma unroll
           for (int i = n - 1; i >= 0; --i) {
+            if (i > lim) continue;
             double acc = 0.0;
 #pragma unroll
             for (int j = 0; j <= i; ++j) acc = fma(s[j], v[i - j], acc);
@@ -276,10 +293,12 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
     };
 
     // Y <- av Lap X (truncated second derivatives, jet_differentiate twice per axis)
-    auto av_lap = [&](const double* X, double* Y) {
+    auto av_lap = [&](const double* X, double* Y, auto limc) {
+      constexpr int lim = decltype(limc)::value;
 #pragma unroll 4
       for (int e = lane; e < E; e += 32) {
         const int q[3] = {e / (n * n), (e / n) % n, e % n};
+        if (q[0] > lim || q[1] > lim || q[2] > lim) continue;
         double acc = 0.0;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
@@ -325,15 +344,20 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
         if (e < E) A[pidx<MM>(e / (n * n), (e / n) % n, e % n)] = dsum[j];
       }
       __syncwarp();
-#pragma unroll 1
-      for (int r = 1; r < n; r += 2) {
-        if (r > 1) {
-          av_lap(A, Cb);  // Cb = av Lap P_{r-2}
+      // levels unrolled so that each level's box is a compile-time bound
+      static_for<0, n / 2>([&](auto ri) {
+        constexpr int r = 2 * decltype(ri)::value + 1;
+        // P_r is read by the target (o <= m) and, through Lap, by P_{r+2}:
+        // box q <= m + (n - 1 - r)
+        constexpr int lim = (MM + (n - 1 - r)) < n - 1 ? MM + (n - 1 - r) : n - 1;
+        using L = std::integral_constant<int, lim>;
+        if constexpr (r > 1) {
+          av_lap(A, Cb, L{});  // Cb = av Lap P_{r-2}
           double* tmp = A;
           A = Cb;
           Cb = tmp;
         }
-        ap_times(A);      // A = P_r
+        ap_times(A, L{});      // A = P_r
         const double w = P.w[r];
 #pragma unroll
         for (int j = 0; j < FL; ++j) {
@@ -343,14 +367,14 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
             tgt[0][j] = fma(w, A[pidx<MM>(o[0], o[1], o[2])], tgt[0][j]);
           }
         }
-      }
+      });
     } else {
       gather_load(0, gbuf);
       reconstruct(-1);  // P_0 in Cb
       double* Pc = Cb;
       double* Xs = A;
-#pragma unroll 1
-      for (int r = 1; r < n; r += 2) {
+      static_for<0, n / 2>([&](auto ri) {
+        constexpr int r = 2 * decltype(ri)::value + 1;
         // V_c[r] = av d_c P_{r-1}: this lane's output entries
         const double w = P.w[r];
 #pragma unroll
@@ -366,14 +390,18 @@ __global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_co
               tgt[c][j] = fma(w, P.av * dv, tgt[c][j]);  // qc + 1 <= m + 1 < n: never truncated here
             }
           }
-        if (r + 2 < n) {
-          av_lap(Pc, Xs);   // Xs = av Lap P_{r-1}
-          ap_times(Xs);     // Xs = P_{r+1}
+        if constexpr (r + 2 < n) {
+          // P_{r+1} is read by V[r+2] = d_c P_{r+1} (o + e_c, o <= m) and,
+          // through Lap, by P_{r+3}: box q <= m + 1 + (n - 2 - (r + 1))
+          constexpr int lim = (MM + 1 + (n - 3 - r)) < n - 1 ? MM + 1 + (n - 3 - r) : n - 1;
+          using L = std::integral_constant<int, lim>;
+          av_lap(Pc, Xs, L{});   // Xs = av Lap P_{r-1}
+          ap_times(Xs, L{});     // Xs = P_{r+1}
           double* tmp = Pc;
           Pc = Xs;
           Xs = tmp;
         }
-      }
+      });
       // keep A/B/Cb roles consistent for the next node
       (void)Xs;
     }
