@@ -102,7 +102,10 @@ template <int MM, int KIND>
 #ifndef HLF_V3_MINB
 #define HLF_V3_MINB 2  // 8 warps per SM with the unrolled line loops beat 16 register-capped ones: 4.9 -> 7.4e9 DOF/s at 192^3 m = 3
 #endif
-__global__ void __launch_bounds__(WARPS * 32, HLF_V3_MINB) var3d(const __grid_constant__ V3Params Q) {
+#ifndef HLF_V3_MINB_M1
+#define HLF_V3_MINB_M1 4  // m = 1: 16 warps per SM (<= 128 registers): 24.3 -> 22.9 ms/step at 192^3 (m = 2, 3: slower)
+#endif
+__global__ void __launch_bounds__(WARPS * 32, MM == 1 ? HLF_V3_MINB_M1 : HLF_V3_MINB) var3d(const __grid_constant__ V3Params Q) {
   using C = V3<MM>;
   constexpr int n1 = C::n1, n = C::n, F = C::F, E = C::E, T = C::T;
   constexpr int NOUT = KIND == VEL ? 3 : 1;
