@@ -97,6 +97,22 @@ def test_tma_path_3d_parity(m, boundary, kx):
     assert g.times() == o.get_times()
 
 
+@pytest.mark.parametrize("raster", ["8", "3", "0"])
+@pytest.mark.parametrize("boundary,kx", [([0, 0, 0], 96), ([1, 1, 1], 95)])
+def test_tma_path_3d_raster_groups(raster, boundary, kx, monkeypatch):
+    """CTA row groups (kernels_tiled3d.cu TParams.raster, default 8 at m = 3)
+    with a partial last group (K_y = 13 = 8 + 5; 3 + 3 + 3 + 3 + 1) cover
+    every CTA exactly once: oracle parity over 6 steps for each grouping."""
+    monkeypatch.setenv("HLF_RASTER", raster)  # read by the host at every launch
+    K = [kx, 13, 20]
+    g, o, _ = setup(3, 3, K, boundary, seed=700 + int(raster))
+    assert g.kernel_variant == 1
+    run([g, o], 6, 0.25 * g.grid.h)
+    for f in range(4):
+        e = rel_err(g.get_field(f), o.get_field(f))
+        assert e <= TOL, (raster, f, e)
+
+
 @pytest.mark.parametrize("m", [1, 2, 3, 4])
 @pytest.mark.parametrize("boundary,kx", [([0, 0], 96), ([1, 1], 96), ([1, 0], 95), ([0, 1], 96)])
 def test_tma_path_2d_parity(m, boundary, kx):
