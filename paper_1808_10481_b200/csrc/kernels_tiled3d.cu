@@ -57,7 +57,7 @@ constexpr int NTHREADS = NWARP * 32;
 #endif
 constexpr int ZC = HLF_ZC;      // target layers per CTA (with TMA loads: 64 +0.9 % over 128, 256 -1.5 %)
 constexpr int kMaxB = 20;       // multi-indices |b| <= 3
-constexpr int kRZ = 2 * 10 * 2 * 4;  // z-folded CK rows: [PZo][(a, b), a + b <= 3][jzo][l] (m = 3)
+constexpr int kRZ = 2 * 10 * 2 * 4;  // z-folded CK rows: [PZo][(a, b), a + b <= m][jzo][l] (sized for m = 3)
 
 template <int MM>
 struct Cfg {
@@ -111,7 +111,7 @@ struct TParams {
   double ML[kMaxN * (kMaxM + 1)];  // s! * M[s][l], l < m+1 (left block), row-major [s][l]
   double GM[kMaxB];                // G_k * k!/b!, indexed by bindex(b)
   double IF[kMaxM + 1];            // 1/o!
-  double RZ[kRZ];                  // pressure launches, m = 3: z sweep folded into the CK (rz_table)
+  double RZ[kRZ];                  // pressure launches, m = 2, 3: z sweep folded into the CK (rz_table)
   const double* src;               // source field base (layer 0 of the allocation)
   const double* src2;              // NT == 2, 4: the V_y source
   const double* src3;              // NT == 4: the V_z source
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
   // but the velocity launch, with three CK bodies and the z-shift selects of
   // its z component, is faster in the plain one-class-per-warp layout
   // (62.2 vs 68.8 ms at 512x512x256).  HLF_NO_V7 / HLF_V7 force one layout.
-  // ZF (m = 3 pressure launches): the z sweep folded into the CK
+  // ZF (m = 2, 3 pressure launches): the z sweep folded into the CK
   // (tiled3d_gen.cuh m3_zf_*: 4 FMAs per (ring column, output) from the
   // column's sum / difference values and the host rows RZ, instead of the z
   // half line plus the CK terms; one output class per warp, the plain
@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(NTHREADS, MM == 1 ? HLF_M1_CTAS : (MM == 2 ? 2
       // Z stage + CK for this warp's parity class
       double pt[nh][nh][nh];
       // ZF runs the merged launch and the V_z launch (the only pressure
-      // launches at m = 3 unless HLF_NO_ZF: launch_m ignores HLF_NO_MERGE)
+      // launches at m = 2, 3 unless HLF_NO_ZF: launch_m ignores HLF_NO_MERGE)
       constexpr bool zf = ZF;
       if constexpr (V7 && !V7S) v7_m3_z(ro + cbase, rn + cbase, cz, zg, pt);
       else if constexpr (!V7) {
