@@ -69,3 +69,32 @@ def test_slab_group_rejects_bad_splits():
         SlabGroup((64, 4, 12), 2.0 / 64, 3, [0] * 5)  # 12 layers do not split into 5
     with pytest.raises(H.ConfigError):
         SlabGroup((64, 4, 12), 2.0 / 64, 3, [0, 0], transport=TRANSPORT_NCCL)  # NCCL: one device per slab
+
+
+def test_eight_slabs_match_one_domain():
+    """The 8-GPU decomposition of BASELINE.json config 5 (8 z slabs, a
+    periodic ring of halo exchanges), all slabs on one GPU with peer copies:
+    bit-exact against one domain over 4 steps (K_z = 16: 2 layers per slab, so
+    every layer is a halo layer for a neighbour)."""
+    global K
+    saved = K
+    K = [64, 4, 16]
+    try:
+        n = 8
+        h = 2.0 / K[0]
+        dt = 0.25 * h
+        g = SlabGroup(tuple(K), h, M_ORDER, [0] * n, transport=TRANSPORT_COPY)
+        st = state()
+        kz = K[2] // n
+        for r in range(n):
+            for f in range(4):
+                g.set_field(r, f, slab(st[f], r * kz, kz))
+        g.set_times(0.0, dt / 2, dt)
+        g.advance_n(4)
+        full = reference(4, dt)
+        for f in range(4):
+            ref = full.get_field(f)
+            for r in range(n):
+                assert np.array_equal(g.get_field(r, f), slab(ref, r * kz, kz)), (f, r)
+    finally:
+        K = saved
