@@ -1,5 +1,5 @@
 """The z-slab decomposition (paper_1808_10481_b200/distributed.py) on CPU:
-world_size 2, 3 and 4 over gloo (3 and 4 make prev != next, so a swapped
+world_size 2, 3, 4 and 8 over gloo (3 and 4 make prev != next, so a swapped
 send / receive direction cannot pass), each rank stepping its slab with the oracle (as the
 compute backend) through the product's HaloExchanger / slab_step logic; the
 gathered result must equal a single-domain run bit for bit (SURVEY.md
@@ -19,7 +19,7 @@ import oracle as O
 from paper_1808_10481_b200.distributed import HaloExchanger, slab_step
 
 M_ORDER = 2
-K = [6, 5, 12]  # z divisible by 2, 3 and 4
+K = [6, 5, 24]  # z divisible by 2, 3, 4 and 8
 
 
 def full_state(seed=11):
@@ -129,7 +129,7 @@ def single_domain(steps):
     return [o.get_field(f) for f in range(4)]
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_slab_decomposition_matches_single_domain(world):
     steps = 3
     results = run_slabs(world, steps)
