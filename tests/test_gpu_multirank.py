@@ -20,7 +20,7 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 M_ORDER = 3
-K = [36, 4, 12]  # z divisible by 2, 3 and 4
+K = [36, 4, 24]  # z divisible by 2, 3, 4 and 8
 
 
 def _state(seed=5):
@@ -89,7 +89,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("overlap", [True, False])
 def test_ranks_on_one_gpu_match_single_domain(world, overlap):
     import paper_1808_10481_b200 as H
