@@ -335,10 +335,41 @@ def main():
         cells = NX * NY * nz
         roofline = roofline_block(kt, pk, cells, ms, dof_local)
 
-        # end to end through the C-ABI with pinned host buffers
+        # end to end through the C-ABI with pinned host buffers (every rank
+        # its slab; N > 1 only when the node's host memory holds all ranks'
+        # pinned states, 128 GiB each at the default size)
         e2e = None
-        if not args.no_e2e and world == 1:
-            e2e = st.e2e(args.e2e_steps, dof_local)
+        e2e_note = None
+        if not args.no_e2e:
+            ok = True
+            if world > 1:
+                need = world * dof_local * 8 * 1.15
+                try:
+                    with open("/proc/meminfo") as f:
+                        avail = next(int(l.split()[1]) * 1024 for l in f if l.startswith("MemAvailable:"))
+                except (OSError, StopIteration, ValueError):
+                    avail = 0
+                flag = torch.tensor([1 if avail >= need else 0], device="cuda")
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                ok = bool(flag.item())
+                if not ok:
+                    e2e_note = (f"e2e skipped: {world} ranks x {dof_local * 8 / 2**30:.0f} GiB of pinned host state "
+                                f"exceed the node's available host memory ({avail / 2**30:.0f} GiB)")
+                else:
+                    dist.barrier()
+            if ok:
+                e2e = st.e2e(args.e2e_steps, dof_local)
+                if world > 1:
+                    t = torch.tensor([e2e["job"]["seconds"]], device="cuda")
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # the slowest rank ends the job
+                    sec = float(t.item())
+                    e2e["job"]["seconds"] = sec
+                    e2e["value"] = dof_total * args.e2e_steps / sec
+                    e2e["h2d_bytes_per_step"] *= world
+                    e2e["d2h_bytes_per_step"] *= world
+                    e2e["job"]["h2d_bytes"] *= world
+                    e2e["job"]["d2h_bytes"] *= world
+                    e2e["job"]["ranks"] = world
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -359,6 +390,7 @@ def main():
             "roofline": roofline,
             "clocks": clk.summary(),
             "e2e": e2e,
+            **({"e2e_note": e2e_note} if e2e_note else {}),
             "cpu_baseline": cpu,
             "finite": bad < 0,
         }
